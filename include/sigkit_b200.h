@@ -1,0 +1,146 @@
+/*
+ * sigkit_b200.h -- C ABI of the B200-native word-basis signature engine.
+ *
+ * This is the drop-in seam for the reference package `sigkit` (paths relative
+ * to /root/reference/pkg/src/sigkit).  The reference crosses from Python into
+ * compiled code at exactly three call sites, all numba kernels that receive
+ * caller-allocated C-contiguous arrays and return nothing:
+ *
+ *   sigcore.py:421   _kernels.forward_kernel(incr, letters, lengths, inv, out)
+ *   sigcore.py:441   _kernels.windows_kernel(incr, letters, lengths, bounds, inv, out)
+ *   backward.py:203  _kernels.backward_kernel(incr, letters, lengths, upstream, inv,
+ *                                            stride, left, right, dh, acc, ckpt, inc_grads)
+ *
+ * plus the word-set tables those kernels consume (wordsets.py:176-247).  The
+ * functions below replace them one for one (see each comment).  Conventions:
+ *
+ *   - every pointer named d_* is DEVICE memory owned by the caller; the
+ *     library never allocates persistent device memory except inside a plan;
+ *   - `stream` is a cudaStream_t passed as void*; all work is enqueued on it;
+ *   - every function returns SIGB_OK (0) or one of the SIGB_ERR_* codes below,
+ *     which the Python layer maps onto the reference's SigkitError hierarchy
+ *     (errors.py:4-37); sigb_last_error() returns the message (thread-local);
+ *   - dtype is SIGB_F32 or SIGB_F64, the dtype of samples/outputs;
+ *   - results are deterministic: no floating-point atomics anywhere, every
+ *     reduction runs in a fixed order (the reference's bitwise
+ *     thread-count-invariance contract, _kernels.py:5-7).
+ */
+#ifndef SIGKIT_B200_H
+#define SIGKIT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SIGB_OK 0
+#define SIGB_ERR_SHAPE 1       /* ShapeError      (errors.py:26) */
+#define SIGB_ERR_DOMAIN 2      /* DomainError     (errors.py:22) */
+#define SIGB_ERR_CAPACITY 3    /* CapacityError   (errors.py:10) */
+#define SIGB_ERR_UNSUPPORTED 4 /* UnsupportedWordSetError (errors.py:34) */
+#define SIGB_ERR_CUDA 5        /* device / launch failure */
+
+#define SIGB_F32 0
+#define SIGB_F64 1
+
+/* ABI version (major * 100 + minor). */
+int sigb_version(void);
+/* Message of the last failing call on this host thread. */
+const char* sigb_last_error(void);
+/* Number of SMs of the current device (grid sizing helper). */
+int sigb_device_sm_count(void);
+
+/*
+ * Word-set tables on device.  Replaces WordSet.letters (wordsets.py:176-188),
+ * WordSet.prefix_table / suffix_table (wordsets.py:190-228, sentinels
+ * EPSILON_INDEX=-1, MISSING_INDEX=-2 at wordsets.py:31-34), the level
+ * offsets behind _level_counts/_level_start/level_slice (wordsets.py:230-247)
+ * and pack_letters (words.py:158-174).  Input: the canonical (length asc,
+ * code asc) arrays WordSet.lengths / WordSet.codes.  Bit-exact with the
+ * reference.  d_packed may be NULL (it needs bits_per_letter*max_len <= 64).
+ *   d_letters     int64 (W, max_len)
+ *   d_prefix      int64 (W, max_len + 1)
+ *   d_suffix      int64 (W, max_len + 1)
+ *   d_level_start int64 (max_len + 2): start of level n at [n], total at [max_len+1]
+ *   d_packed      uint64 (W)
+ */
+int sigb_wordset_tables(const uint64_t* d_codes, const int64_t* d_lengths, int64_t W, int64_t d,
+                        int64_t max_len, int64_t* d_letters, int64_t* d_prefix, int64_t* d_suffix,
+                        int64_t* d_level_start, uint64_t* d_packed, void* stream);
+
+/*
+ * Execution plan of one word set (opaque).  Built from the host copies of
+ * WordSet.codes / WordSet.lengths: computes the prefix closure cl(I) (the
+ * reference computes missing prefixes as scratch, wordsets.py:8-9), runs
+ * sigb_wordset_tables on it, and derives the kernels' schedule (parent /
+ * child / level tables, partition of the trie into independent parts).
+ * Holds device memory until sigb_plan_destroy.
+ */
+typedef struct sigb_plan sigb_plan;
+
+int sigb_plan_create(const uint64_t* codes, const int64_t* lengths, int64_t W, int64_t d,
+                     sigb_plan** plan, void* stream);
+int sigb_plan_destroy(sigb_plan* plan);
+/* |cl(I)| -- width of the closure state used by sigb_backward when I is not prefix-closed. */
+int64_t sigb_plan_closure_size(const sigb_plan* plan);
+/* Number of independent trie parts (diagnostics / DESIGN.md). */
+int64_t sigb_plan_num_parts(const sigb_plan* plan);
+/* Executed FMA count of one Chen step of one path (T-node count; diagnostics). */
+int64_t sigb_plan_step_fmas(const sigb_plan* plan);
+
+/*
+ * Forward signature.  Replaces forward_kernel (_kernels.py:40-58) together
+ * with the increments (sigcore.py:263-271, fused: the kernel differences the
+ * samples itself) and the epsilon column (sigcore.py:401-407).
+ *   d_X      (B, L, d) samples, dtype
+ *   d_out    row b at d_out + b*out_ld; word k of I is written at column out_col0+k;
+ *            if include_empty, column out_col0-1 is set to 1 (needs out_col0 >= 1)
+ *   d_state  NULL, or (B, |cl(I)|) terminal closure state (needed by sigb_backward
+ *            when I is not prefix-closed)
+ * L == 1 (no increments) yields the identity (zeros), as the reference.
+ */
+int sigb_forward(const sigb_plan* plan, int dtype, const void* d_X, int64_t B, int64_t L,
+                 void* d_out, int64_t out_ld, int64_t out_col0, int include_empty, void* d_state,
+                 void* stream);
+
+/*
+ * Windowed signatures.  Replaces windows_kernel (_kernels.py:61-82):
+ * d_bounds int64 (K, 2) sample-index pairs 0 <= l < r <= L-1 (validated by
+ * the caller, sigcore.py:321-346); d_out (B, K, W) -- window k of path b
+ * at d_out + (b*K + k)*W.
+ */
+int sigb_windows(const sigb_plan* plan, int dtype, const void* d_X, int64_t B, int64_t L,
+                 const int64_t* d_bounds, int64_t K, void* d_out, void* stream);
+
+/*
+ * Backward.  Replaces backward_kernel (_kernels.py:85-183) fused with
+ * increment_to_sample_grads (backward.py:130-147).  Memory-lean: consumes
+ * the terminal signature instead of a stored trajectory and rebuilds
+ * S_{0,t_j} by multiplying with exp(-dX_j) while sweeping j = M-1..0.
+ *   d_S      terminal state: (B, W) forward output (out_ld/out_col0 layout of
+ *            sigb_forward) when I is prefix-closed, else the d_state (B, |cl(I)|)
+ *            of sigb_forward (set s_is_state = 1)
+ *   d_g      upstream dL/dS, row b at d_g + b*g_ld, word k at column g_col0 + k
+ *            (a leading epsilon column is skipped by passing g_col0 = 1,
+ *            backward.py:177-178)
+ *   ckpt_stride  0 = pure reconstruction; c > 0 = reload exact S_{0,t_j}
+ *            every c steps from checkpoints taken by a forward replay
+ *            (the reference's accuracy dial, backward.py:183-199)
+ *   d_work   workspace of sigb_backward_workspace_size bytes
+ *   d_dX     (B, L, d) dL/dX, dtype (the path gradients, fully overwritten)
+ *   d_dinc   NULL or (B, L-1, d) dL/d(dX_j) (GradBatch.increment_grads)
+ */
+int sigb_backward_workspace_size(const sigb_plan* plan, int dtype, int64_t B, int64_t L,
+                                 int64_t ckpt_stride, size_t* bytes);
+int sigb_backward(const sigb_plan* plan, int dtype, const void* d_X, int64_t B, int64_t L,
+                  const void* d_S, int64_t s_ld, int64_t s_col0, int s_is_state, const void* d_g,
+                  int64_t g_ld, int64_t g_col0, int64_t ckpt_stride, void* d_work, size_t work_bytes,
+                  void* d_dX, void* d_dinc, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SIGKIT_B200_H */

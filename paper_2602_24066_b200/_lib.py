@@ -1,0 +1,79 @@
+"""ctypes binding of the C ABI in include/sigkit_b200.h (libsigkit_b200.so).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (or
+``python -m paper_2602_24066_b200.build``).  There is no fallback: if the
+library or a CUDA device is missing every compute call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from . import exceptions as E
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsigkit_b200.so")
+
+SIGB_OK = 0
+SIGB_F32 = 0
+SIGB_F64 = 1
+
+_ERRORS = {
+    1: E.ShapeError,
+    2: E.DomainError,
+    3: E.CapacityError,
+    4: E.UnsupportedWordSetError,
+}
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int64
+_C = ctypes.c_int
+
+# name -> (restype, argtypes); mirrors include/sigkit_b200.h
+SIGNATURES = {
+    "sigb_version": (ctypes.c_int, []),
+    "sigb_last_error": (ctypes.c_char_p, []),
+    "sigb_device_sm_count": (ctypes.c_int, []),
+    "sigb_wordset_tables": (_C, [_P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
+    "sigb_plan_create": (_C, [_P, _P, _I, _I, ctypes.POINTER(_P), _P]),
+    "sigb_plan_destroy": (_C, [_P]),
+    "sigb_plan_closure_size": (_I, [_P]),
+    "sigb_plan_num_parts": (_I, [_P]),
+    "sigb_plan_step_fmas": (_I, [_P]),
+    "sigb_forward": (_C, [_P, _C, _P, _I, _I, _P, _I, _I, _C, _P, _P]),
+    "sigb_windows": (_C, [_P, _C, _P, _I, _I, _P, _I, _P, _P]),
+    "sigb_backward_workspace_size": (_C, [_P, _C, _I, _I, _I, ctypes.POINTER(ctypes.c_size_t)]),
+    "sigb_backward": (_C, [_P, _C, _P, _I, _I, _P, _I, _I, _C, _P, _I, _I, _I, _P, ctypes.c_size_t,
+                           _P, _P, _P]),
+}
+
+_lib = None
+
+
+class ExtensionMissing(RuntimeError):
+    """The CUDA extension was not built or cannot be loaded."""
+
+
+def lib():
+    """Load libsigkit_b200.so once; raise loudly if it is absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ExtensionMissing(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == SIGB_OK:
+        return
+    msg = lib().sigb_last_error().decode(errors="replace")
+    raise _ERRORS.get(rc, RuntimeError)(msg)

@@ -1,0 +1,55 @@
+"""Build libsigkit_b200.so in-tree: nvcc for sm_100a, static cudart, -lineinfo.
+
+    python -m paper_2602_24066_b200.build
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "libsigkit_b200.so")
+SOURCES = ["sigb_api.cu", "sigb_plan.cu", "sigb_tables.cu"]
+DEPS = SOURCES + ["sigb_internal.h", "sigb_level.cu", "sigb_trunc.cuh"]
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
+    "-Xptxas", "-v",
+]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if cand and (os.path.exists(cand) or cand == "nvcc"):
+            return cand
+    return "nvcc"
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    srcs = [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
+    deps = [os.path.join(CSRC, s) for s in DEPS if os.path.exists(os.path.join(CSRC, s))]
+    deps.append(os.path.join(HERE, "..", "include", "sigkit_b200.h"))
+    if not force and os.path.exists(OUT):
+        mt = os.path.getmtime(OUT)
+        if all(os.path.getmtime(p) <= mt for p in deps):
+            return OUT
+    cmd = [nvc for nvc in [nvcc()]] + NVCC_FLAGS + ["-o", OUT] + srcs
+    res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+    log = os.path.join(CSRC, "build.log")
+    with open(log, "w") as f:
+        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"nvcc failed ({res.returncode}); see {log}")
+    if verbose:
+        sys.stdout.write(res.stdout + res.stderr)
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

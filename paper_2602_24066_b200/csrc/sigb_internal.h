@@ -1,0 +1,96 @@
+// Internal definitions shared by the sigkit_b200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/sigkit_b200.h"
+
+namespace sigb {
+
+// Longest word the device kernels schedule (level tables are fixed-size).
+constexpr int kMaxLevel = 32;
+// Steps of samples staged in shared memory per chunk.
+constexpr int kChunk = 32;
+
+// Records `msg` as the thread's last error and returns `code`.
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+
+#define SIGB_CUDA_TRY(expr)                                   \
+  do {                                                        \
+    cudaError_t _e = (expr);                                  \
+    if (_e != cudaSuccess) return ::sigb::cuda_fail(_e, #expr); \
+  } while (0)
+
+// One independent part of the trie: a run of consecutive sibling subtrees
+// plus the (replicated) chain of their common ancestors.  Local node order is
+// canonical (level asc, code asc), so every level is a contiguous local range.
+struct PartDesc {
+  int n;         // local nodes (chain + subtrees)
+  int node_off;  // offset into the node tables
+  int tv_size;   // T-vector entries T(w, m), m > |w|
+  int tb_size;   // adjoint entries Tbar(w, m), m >= |w|
+  int lseg_off;  // offset into the letter-segment table (d + 1 entries)
+  int depth;     // deepest level present
+  int lvl[kMaxLevel + 2];  // lvl[l] = first local node of level l (1-based), lvl[depth+1] = n
+};
+
+// Node table entry A: {parent T-vector offset (-1: parent is the empty word),
+//  letter | level << 8 | maxdesc << 16 | owner << 24, own T-vector offset (-1: none),
+//  own adjoint offset}
+// Node table entry B: {closure index, emitted index in I (-1: closure only),
+//  first child (local), child count}.  Only the owner part emits / seeds a node.
+struct PlanDev {
+  const PartDesc* parts;
+  const int4* nodeA;
+  const int4* nodeB;
+  const int* perm;  // per part: local ids sorted by (letter, id)
+  const int* lseg;  // per part: d + 1 segment starts into perm
+  int num_parts;
+  int d;
+  int max_len;
+};
+
+}  // namespace sigb
+
+struct sigb_plan {
+  int64_t d = 0;
+  int64_t W = 0;   // emitted words |I|
+  int64_t Wc = 0;  // closure |cl(I)|
+  int max_len = 0;
+  bool prefix_closed = true;
+  int num_parts = 0;
+  int64_t step_fmas = 0;
+  // per-dtype-agnostic smem requirements (in elements of the compute type)
+  int max_n = 0, max_tv = 0, max_tb = 0;
+  // device arrays
+  sigb::PartDesc* d_parts = nullptr;
+  int4* d_nodeA = nullptr;
+  int4* d_nodeB = nullptr;
+  int* d_perm = nullptr;
+  int* d_lseg = nullptr;
+  std::vector<sigb::PartDesc> h_parts;
+
+  sigb::PlanDev dev() const {
+    sigb::PlanDev p;
+    p.parts = d_parts;
+    p.nodeA = d_nodeA;
+    p.nodeB = d_nodeB;
+    p.perm = d_perm;
+    p.lseg = d_lseg;
+    p.num_parts = num_parts;
+    p.d = (int)d;
+    p.max_len = max_len;
+    return p;
+  }
+};
+
+namespace sigb {
+int launch_wordset_tables(const uint64_t* d_codes, const int64_t* d_lengths, int64_t W, int64_t d,
+                          int64_t max_len, int64_t* d_letters, int64_t* d_prefix, int64_t* d_suffix,
+                          int64_t* d_level_start, uint64_t* d_packed, cudaStream_t stream);
+}  // namespace sigb

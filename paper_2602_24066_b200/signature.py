@@ -1,0 +1,247 @@
+"""Forward signatures: the reference's public forward API on the B200 kernels.
+
+Mirrors /root/reference/pkg/src/sigkit/sigcore.py:36-263 (PathBatch,
+CoefficientBatch, WindowSpec, signature_forward, signature_windows and the
+scalar reference formulas).  numpy in -> numpy out (host buffers are staged
+through pinned memory); a CUDA torch tensor in -> tensor values out, on the
+tensor's device and stream.  All arithmetic runs in ``sigb_forward`` /
+``sigb_windows`` (csrc/sigb_level.cu).
+"""
+
+from __future__ import annotations
+
+import functools
+import math
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from .device import resolve_device
+from .exceptions import DomainError, ShapeError, WindowError
+from .wordcodes import Word, decode_word
+from .wordset import WordSet
+
+SUPPORTED_DTYPES = (np.float64, np.float32)
+
+
+def _is_tensor(x) -> bool:
+    return isinstance(x, torch.Tensor)
+
+
+class PathBatch:
+    """B paths of M+1 samples in R^d (sigcore.py:36-88); validates like the reference."""
+
+    def __init__(self, samples, dtype=None, allow_nonfinite: bool = False):
+        if _is_tensor(samples):
+            arr = samples
+            if dtype is not None:
+                arr = arr.to(torch.float64 if np.dtype(dtype) == np.float64 else torch.float32)
+            elif arr.dtype not in (torch.float32, torch.float64):
+                arr = arr.to(torch.float64)
+            if arr.dim() != 3:
+                raise ShapeError(f"samples must have shape (B, M+1, d), got {tuple(arr.shape)}")
+            if arr.shape[1] < 1:
+                raise ShapeError("paths need at least one sample point")
+            if not allow_nonfinite and arr.numel() and not bool(torch.isfinite(arr).all()):
+                raise DomainError("samples contain non-finite values; pass allow_nonfinite=True to propagate them")
+            self.samples = arr.contiguous()
+            return
+        arr = np.asarray(samples)
+        if dtype is not None:
+            arr = arr.astype(dtype, copy=False)
+        elif arr.dtype not in SUPPORTED_DTYPES:
+            arr = arr.astype(np.float64)
+        if arr.dtype not in SUPPORTED_DTYPES:
+            raise ShapeError(f"unsupported dtype {arr.dtype}; use float64 or float32")
+        if arr.ndim != 3:
+            raise ShapeError(f"samples must have shape (B, M+1, d), got {arr.shape}")
+        if arr.shape[1] < 1:
+            raise ShapeError("paths need at least one sample point")
+        if not allow_nonfinite and not np.all(np.isfinite(arr)):
+            raise DomainError("samples contain non-finite values; pass allow_nonfinite=True to propagate them")
+        self.samples = np.ascontiguousarray(arr)
+
+    @property
+    def B(self) -> int:
+        return int(self.samples.shape[0])
+
+    @property
+    def M(self) -> int:
+        return int(self.samples.shape[1]) - 1
+
+    @property
+    def d(self) -> int:
+        return int(self.samples.shape[2])
+
+    @property
+    def dtype(self):
+        if _is_tensor(self.samples):
+            return np.float64 if self.samples.dtype == torch.float64 else np.float32
+        return self.samples.dtype
+
+    @functools.cached_property
+    def increments(self):
+        s = self.samples
+        return s[:, 1:] - s[:, :-1]
+
+
+def as_path_batch(paths, dtype=None) -> PathBatch:
+    return paths if isinstance(paths, PathBatch) else PathBatch(paths, dtype=dtype)
+
+
+@dataclass
+class CoefficientBatch:
+    """Signature coefficients over a WordSet; column k is wordset word k (+ leading eps)."""
+
+    wordset: WordSet
+    values: object
+
+    def __post_init__(self):
+        shape = tuple(self.values.shape)
+        if len(shape) != 2 or shape[1] != self.wordset.width:
+            raise ShapeError(f"coefficient values must have shape (B, {self.wordset.width}), got {shape}")
+
+    @property
+    def B(self) -> int:
+        return int(self.values.shape[0])
+
+    @property
+    def width(self) -> int:
+        return int(self.values.shape[1])
+
+    @property
+    def word_values(self):
+        return self.values[:, 1:] if self.wordset.include_empty else self.values
+
+    def column_names(self) -> list[str]:
+        names = self.wordset.word_strings()
+        return ["e"] + names if self.wordset.include_empty else names
+
+    def __array__(self, dtype=None, copy=None):
+        v = self.values.cpu().numpy() if _is_tensor(self.values) else self.values
+        return np.asarray(v, dtype=dtype)
+
+
+@dataclass(frozen=True)
+class WindowSpec:
+    """K windows (l, r) over the sample axis, 0 <= l < r (sigcore.py:138-163)."""
+
+    pairs: np.ndarray
+
+    def __post_init__(self):
+        arr = np.ascontiguousarray(np.asarray(self.pairs, dtype=np.int64))
+        if arr.ndim != 2 or arr.shape[1] != 2:
+            raise WindowError(f"window pairs must have shape (K, 2), got {arr.shape}")
+        object.__setattr__(self, "pairs", arr)
+        if arr.shape[0] == 0:
+            raise WindowError("need at least one window")
+        if np.any(arr[:, 0] < 0) or np.any(arr[:, 0] >= arr[:, 1]):
+            raise WindowError("windows must satisfy 0 <= l < r")
+
+    @property
+    def K(self) -> int:
+        return int(self.pairs.shape[0])
+
+    def validate_for(self, M: int) -> None:
+        over = self.pairs[:, 1] > M
+        if np.any(over):
+            l, r = self.pairs[over][0]
+            raise WindowError(f"window ({l}, {r}) exceeds the last sample index {M}")
+
+
+# -- scalar reference formulas (sigcore.py:169-195); host-side, for tests --------------
+
+
+def segment_exp_coeff(delta: Sequence[float], w: Word) -> float:
+    """<exp(delta), w> = prod_j delta[w_j] / |w|!."""
+    p = 1.0
+    for x in decode_word(w, len(delta)):
+        p *= float(delta[x])
+    return p / math.factorial(w.length)
+
+
+def horner_update(prev: Sequence[float], delta: Sequence[float], w: Word) -> float:
+    """One Horner-form Chen step for word w from its prefix values prev[0..|w|]."""
+    letters = decode_word(w, len(delta))
+    n = w.length
+    if len(prev) != n + 1:
+        raise ShapeError(f"need {n + 1} prefix values, got {len(prev)}")
+    h = 0.0
+    for k, x in enumerate(letters):
+        h = float(delta[x]) / (n - k) * (float(prev[k]) + h)
+    return float(prev[n]) + h
+
+
+# -- batched forward ---------------------------------------------------------------------
+
+
+def _check_compute(paths: PathBatch, ws: WordSet) -> None:
+    if len(ws) < 1:
+        raise DomainError("word set has no words to compute")
+    if ws.d != paths.d:
+        raise ShapeError(f"word set has d={ws.d} but paths have {paths.d} channels")
+
+
+def to_device(samples, device) -> torch.Tensor:
+    """Host numpy -> device tensor through pinned memory (or pass a CUDA tensor through)."""
+    if _is_tensor(samples):
+        return samples.to(device).contiguous()
+    host = torch.from_numpy(np.ascontiguousarray(samples))
+    if host.numel() and torch.cuda.is_available():
+        host = host.pin_memory()
+    return host.to(device, non_blocking=True)
+
+
+def forward_tensor(X: torch.Tensor, ws: WordSet, want_state: bool = False):
+    """(out (B, width), closure state or None) for a CUDA tensor X (B, L, d)."""
+    plan = ws.plan(X.device)
+    B = X.shape[0]
+    out = torch.empty((B, ws.width), dtype=X.dtype, device=X.device)
+    state = None
+    if want_state and not plan.prefix_closed:
+        state = torch.empty((B, plan.Wc), dtype=X.dtype, device=X.device)
+    plan.forward(X, out, 1 if ws.include_empty else 0, ws.include_empty, state)
+    return out, state
+
+
+def signature_forward(paths, ws: WordSet, threads: int | None = None) -> CoefficientBatch:
+    """Signature coefficients of each path at every word of the set (sigcore.py:410-422).
+
+    ``threads`` is accepted for API compatibility; the GPU grid is fixed by the plan.
+    """
+    paths = as_path_batch(paths)
+    _check_compute(paths, ws)
+    if _is_tensor(paths.samples):
+        X = paths.samples
+        dev = resolve_device(X.device if X.is_cuda else None)
+        out, _ = forward_tensor(X.to(dev), ws)
+        return CoefficientBatch(ws, out)
+    dev = resolve_device()
+    X = to_device(paths.samples, dev)
+    out, _ = forward_tensor(X, ws)
+    return CoefficientBatch(ws, out.cpu().numpy())
+
+
+def signature_windows(paths, ws: WordSet, windows, threads: int | None = None) -> list[CoefficientBatch]:
+    """Independent signatures of K sample windows (sigcore.py:425-446)."""
+    paths = as_path_batch(paths)
+    _check_compute(paths, ws)
+    if not isinstance(windows, WindowSpec):
+        windows = WindowSpec(np.asarray(windows))
+    windows.validate_for(paths.M)
+    is_t = _is_tensor(paths.samples)
+    dev = resolve_device(paths.samples.device if is_t and paths.samples.is_cuda else None)
+    X = to_device(paths.samples, dev)
+    bounds = torch.from_numpy(windows.pairs).to(dev)
+    plan = ws.plan(dev)
+    out = torch.empty((paths.B, windows.K, len(ws)), dtype=X.dtype, device=dev)
+    plan.windows(X, bounds, out)
+    res = []
+    for k in range(windows.K):
+        v = out[:, k, :]
+        if ws.include_empty:
+            v = torch.cat([torch.ones((paths.B, 1), dtype=X.dtype, device=dev), v], dim=1)
+        res.append(CoefficientBatch(ws, v if is_t else v.cpu().numpy()))
+    return res
