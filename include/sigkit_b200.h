@@ -51,6 +51,12 @@ int sigb_version(void);
 const char* sigb_last_error(void);
 /* Number of SMs of the current device (grid sizing helper). */
 int sigb_device_sm_count(void);
+/* Kernel routing: 0 = auto (register-resident truncated kernels where an
+ * instantiation exists, generic trie kernels otherwise), 1 = generic only.
+ * Process-wide; used by the tests to check both paths against the oracle. */
+int sigb_set_kernel_policy(int policy);
+/* Number of device kernels this library has launched (process-wide). */
+long long sigb_launch_count(void);
 
 /*
  * Word-set tables on device.  Replaces WordSet.letters (wordsets.py:176-188),

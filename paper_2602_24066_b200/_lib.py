@@ -35,6 +35,8 @@ SIGNATURES = {
     "sigb_version": (ctypes.c_int, []),
     "sigb_last_error": (ctypes.c_char_p, []),
     "sigb_device_sm_count": (ctypes.c_int, []),
+    "sigb_set_kernel_policy": (_C, [_C]),
+    "sigb_launch_count": (ctypes.c_longlong, []),
     "sigb_wordset_tables": (_C, [_P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     "sigb_plan_create": (_C, [_P, _P, _I, _I, ctypes.POINTER(_P), _P]),
     "sigb_plan_destroy": (_C, [_P]),
@@ -77,3 +79,12 @@ def check(rc: int) -> None:
         return
     msg = lib().sigb_last_error().decode(errors="replace")
     raise _ERRORS.get(rc, RuntimeError)(msg)
+
+
+def set_kernel_policy(policy: int) -> None:
+    """0 = auto (register-resident truncated kernels where available), 1 = generic trie kernels only."""
+    check(lib().sigb_set_kernel_policy(int(policy)))
+
+
+def launch_count() -> int:
+    return int(lib().sigb_launch_count())

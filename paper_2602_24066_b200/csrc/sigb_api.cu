@@ -1,6 +1,7 @@
 // C ABI entry points (include/sigkit_b200.h): validation, launch geometry,
 // batch chunking of the backward workspace.
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 
 #include "sigb_internal.h"
@@ -9,6 +10,9 @@
 namespace sigb {
 
 static thread_local std::string g_last_error;
+int g_policy = 0;
+static std::atomic<long long> g_launches{0};
+void count_launch(int n) { g_launches += n; }
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -56,6 +60,7 @@ int forward_t(const sigb_plan* p, const void* X, int64_t B, int64_t L, const int
   SIGB_CUDA_TRY(cudaFuncSetAttribute(forward_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t grid = B * K * p->num_parts;
   if (grid == 0) return SIGB_OK;
+  count_launch();
   forward_kernel<T><<<(unsigned)grid, kThreads, smem, stream>>>(
       p->dev(), (const T*)X, L, bounds, K, (T*)out, out_ld, out_col0, include_empty, (T*)state, p->Wc, ckpt,
       stride, nck, p->max_n);
@@ -108,6 +113,7 @@ int backward_t(const sigb_plan* p, const void* X, int64_t B, int64_t L, const vo
                         geo.nck, stream);
       if (rc) return rc;
     }
+    count_launch(2);
     backward_kernel<T><<<(unsigned)(Bc * p->num_parts), kThreads, smem, stream>>>(
         p->dev(), (const T*)X, L, b0, (const T*)S, s_ld, s_col0, s_is_state, p->Wc, (const T*)g, g_ld, g_col0,
         ckpt, stride, geo.nck, p->max_n, partial);
@@ -119,6 +125,8 @@ int backward_t(const sigb_plan* p, const void* X, int64_t B, int64_t L, const vo
   }
   return SIGB_OK;
 }
+
+bool use_trunc(const sigb_plan* p) { return g_policy == 0 && p->trunc_depth >= 2 && trunc::supported(p->d, p->trunc_depth); }
 
 int check_common(const sigb_plan* p, int dtype, int64_t B, int64_t L) {
   if (!p) return fail(SIGB_ERR_DOMAIN, "plan is NULL");
@@ -134,6 +142,12 @@ int check_common(const sigb_plan* p, int dtype, int64_t B, int64_t L) {
 using namespace sigb;
 
 extern "C" int sigb_version(void) { return 100; }
+extern "C" int sigb_set_kernel_policy(int policy) {
+  if (policy < 0 || policy > 1) return fail(SIGB_ERR_DOMAIN, "kernel policy must be 0 (auto) or 1 (generic)");
+  g_policy = policy;
+  return SIGB_OK;
+}
+extern "C" long long sigb_launch_count(void) { return g_launches.load(); }
 extern "C" const char* sigb_last_error(void) { return g_last_error.c_str(); }
 
 extern "C" int sigb_device_sm_count(void) {
@@ -155,6 +169,11 @@ extern "C" int sigb_forward(const sigb_plan* plan, int dtype, const void* d_X, i
   int rc = check_common(plan, dtype, B, L);
   if (rc) return rc;
   if (include_empty && out_col0 < 1) return fail(SIGB_ERR_SHAPE, "include_empty needs out_col0 >= 1");
+  if (use_trunc(plan)) {
+    count_launch();
+    return trunc::forward(dtype, plan->d, plan->trunc_depth, d_X, B, L, d_out, out_ld, out_col0, include_empty,
+                          (cudaStream_t)stream);
+  }
   if (dtype == SIGB_F32)
     return forward_t<float>(plan, d_X, B, L, nullptr, 1, d_out, out_ld, out_col0, include_empty, d_state, nullptr, 0,
                             0, (cudaStream_t)stream);
@@ -180,6 +199,10 @@ extern "C" int sigb_backward_workspace_size(const sigb_plan* plan, int dtype, in
   if (rc) return rc;
   if (ckpt_stride < 0) return fail(SIGB_ERR_DOMAIN, "checkpoint stride must be >= 1");
   if (B == 0 || L == 1) { *bytes = 0; return SIGB_OK; }
+  if (use_trunc(plan) && ckpt_stride == 0) {
+    *bytes = trunc::backward_workspace(dtype, plan->d, plan->trunc_depth, B, L);
+    return SIGB_OK;
+  }
   if (dtype == SIGB_F32) {
     BwdGeometry g = bwd_geometry<float>(plan, B, L, ckpt_stride);
     *bytes = g.partial_bytes + g.ckpt_bytes;
@@ -199,6 +222,12 @@ extern "C" int sigb_backward(const sigb_plan* plan, int dtype, const void* d_X, 
   if (ckpt_stride < 0) return fail(SIGB_ERR_DOMAIN, "checkpoint stride must be >= 1");
   if (!s_is_state && !plan->prefix_closed)
     return fail(SIGB_ERR_DOMAIN, "word set is not prefix-closed: pass the closure state from sigb_forward");
+  if (use_trunc(plan) && ckpt_stride == 0 && B > 0 && L > 1) {
+    if (s_is_state) { s_ld = plan->Wc; s_col0 = 0; }
+    count_launch(2);
+    return trunc::backward(dtype, plan->d, plan->trunc_depth, d_X, B, L, d_S, s_ld, s_col0, d_g, g_ld, g_col0, d_work,
+                           work_bytes, d_dX, d_dinc, (cudaStream_t)stream);
+  }
   if (dtype == SIGB_F32)
     return backward_t<float>(plan, d_X, B, L, d_S, s_ld, s_col0, s_is_state, d_g, g_ld, g_col0, ckpt_stride, d_work,
                              work_bytes, d_dX, d_dinc, (cudaStream_t)stream);

@@ -63,6 +63,7 @@ struct sigb_plan {
   int64_t Wc = 0;  // closure |cl(I)|
   int max_len = 0;
   bool prefix_closed = true;
+  int trunc_depth = 0;  // N when cl(I) is the full truncation of depth N, else 0
   int num_parts = 0;
   int64_t step_fmas = 0;
   // per-dtype-agnostic smem requirements (in elements of the compute type)
@@ -90,6 +91,18 @@ struct sigb_plan {
 };
 
 namespace sigb {
+// kernel-routing policy (sigb_set_kernel_policy) and launch counter
+extern int g_policy;
+void count_launch(int n = 1);
+namespace trunc {
+bool supported(int64_t d, int depth);
+int forward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L, void* out, int64_t out_ld,
+            int64_t out_col0, int include_empty, cudaStream_t stream);
+size_t backward_workspace(int dtype, int64_t d, int depth, int64_t B, int64_t L);
+int backward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L, const void* S, int64_t s_ld,
+             int64_t s_col0, const void* g, int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, void* dX,
+             void* dinc, cudaStream_t stream);
+}  // namespace trunc
 int launch_wordset_tables(const uint64_t* d_codes, const int64_t* d_lengths, int64_t W, int64_t d,
                           int64_t max_len, int64_t* d_letters, int64_t* d_prefix, int64_t* d_suffix,
                           int64_t* d_level_start, uint64_t* d_packed, cudaStream_t stream);

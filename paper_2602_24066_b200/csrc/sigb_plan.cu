@@ -166,6 +166,17 @@ extern "C" int sigb_plan_create(const uint64_t* codes, const int64_t* lengths, i
   plan->Wc = Wc;
   plan->max_len = (int)max_len;
   plan->prefix_closed = (Wc == W);
+  {
+    bool full = plan->prefix_closed;
+    std::vector<int64_t> cnt(max_len + 1, 0);
+    for (int64_t i = 0; i < Wc; ++i) cnt[t.len[i]]++;
+    uint64_t p = 1;
+    for (int64_t n = 1; n <= max_len && full; ++n) {
+      p *= (uint64_t)d;
+      full = full && (uint64_t)cnt[n] == p;
+    }
+    plan->trunc_depth = full ? (int)max_len : 0;
+  }
   plan->num_parts = (int)specs.size();
   std::vector<int4> nodeA, nodeB;
   std::vector<int> perm, lseg;

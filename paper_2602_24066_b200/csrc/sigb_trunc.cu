@@ -1,0 +1,153 @@
+// Instantiations and dispatch of the register-resident truncated kernels.
+// A plan whose closure is a full truncation (all D^n words of every length
+// 1..N) is routed here when (D, N) has an instantiation; everything else
+// runs the generic trie kernels of sigb_level.cu.
+#include "sigb_trunc.cuh"
+
+namespace sigb {
+namespace trunc {
+namespace {
+
+constexpr size_t kPartialBudget = size_t(8) << 30;  // bytes of per-part gradient partials per chunk
+
+template <typename T, int D, int N, int G>
+int fwd(const T* X, int64_t B, int64_t L, T* out, int64_t out_ld, int64_t out_col0, int include_empty,
+        cudaStream_t stream) {
+  using C = Cfg<D, N, G>;
+  const int64_t grid = C::CPP > 1 ? B * C::CPP : (B + C::PPC - 1) / C::PPC;
+  if (grid == 0) return SIGB_OK;
+  constexpr size_t smem = sizeof(T) * ((size_t)C::PPC * (kChunkT + 1) * D + (size_t)C::PPC * kChunkT * D);
+  trunc_forward_kernel<T, D, N, G><<<(unsigned)grid, C::THREADS, smem, stream>>>(X, B, L, out, out_ld, out_col0,
+                                                                                include_empty);
+  SIGB_CUDA_TRY(cudaGetLastError());
+  return SIGB_OK;
+}
+
+template <typename T, int D, int N, int G>
+int64_t bwd_chunk(int64_t B, int64_t L) {
+  using C = Cfg<D, N, G>;
+  const size_t per_path = sizeof(T) * (size_t)C::CPP * (L - 1) * D;
+  int64_t chunk = per_path ? (int64_t)(kPartialBudget / per_path) : B;
+  chunk = std::max<int64_t>(C::PPC, chunk - chunk % C::PPC);
+  return std::min<int64_t>(chunk, ((B + C::PPC - 1) / C::PPC) * C::PPC);
+}
+
+template <typename T, int D, int N, int G>
+size_t bwd_workspace(int64_t B, int64_t L) {
+  using C = Cfg<D, N, G>;
+  return sizeof(T) * (size_t)bwd_chunk<T, D, N, G>(B, L) * C::CPP * (L - 1) * D;
+}
+
+template <typename T>
+__global__ void trunc_sample_grads(const T* __restrict__ partial, int64_t Bc, int64_t P, int64_t M, int64_t d,
+                                   int64_t b0, int64_t B, T* __restrict__ dX, T* __restrict__ dinc) {
+  const int64_t L = M + 1;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= Bc * L * d) return;
+  const int64_t z = i % d, t = (i / d) % L, bl = i / (d * L);
+  if (b0 + bl >= B) return;
+  auto inc = [&](int64_t j) {
+    T s = T(0);
+    for (int64_t p = 0; p < P; ++p) s += partial[((bl * P + p) * M + j) * d + z];
+    return s;
+  };
+  T v = T(0);
+  if (t >= 1) v += inc(t - 1);
+  if (t < M) {
+    const T it = inc(t);
+    v -= it;
+    if (dinc) dinc[((b0 + bl) * M + t) * d + z] = it;
+  }
+  dX[((b0 + bl) * L + t) * d + z] = v;
+}
+
+template <typename T, int D, int N, int G>
+int bwd(const T* X, int64_t B, int64_t L, const T* S, int64_t s_ld, int64_t s_col0, const T* g, int64_t g_ld,
+        int64_t g_col0, void* work, size_t work_bytes, T* dX, T* dinc, cudaStream_t stream) {
+  using C = Cfg<D, N, G>;
+  using RG = RedGeom<D, N, G>;
+  const int64_t M = L - 1;
+  const int64_t chunk = bwd_chunk<T, D, N, G>(B, L);
+  if (work_bytes < bwd_workspace<T, D, N, G>(B, L) || !work)
+    return fail(SIGB_ERR_DOMAIN, "backward workspace too small");
+  constexpr size_t smem = RG::template smem_bytes<T>();
+  SIGB_CUDA_TRY(cudaFuncSetAttribute(trunc_backward_kernel<T, D, N, G>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  T* partial = (T*)work;
+  for (int64_t b0 = 0; b0 < B; b0 += chunk) {
+    const int64_t Bc = std::min(chunk, B - b0);
+    const int64_t grid = C::CPP > 1 ? Bc * C::CPP : (Bc + C::PPC - 1) / C::PPC;
+    trunc_backward_kernel<T, D, N, G><<<(unsigned)grid, C::THREADS, smem, stream>>>(
+        X, B, L, b0, S, s_ld, s_col0, g, g_ld, g_col0, partial);
+    SIGB_CUDA_TRY(cudaGetLastError());
+    const int64_t n = Bc * L * D;
+    trunc_sample_grads<T><<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(partial, Bc, C::CPP, M, D, b0, B, dX,
+                                                                           dinc);
+    SIGB_CUDA_TRY(cudaGetLastError());
+  }
+  return SIGB_OK;
+}
+
+// (D, N) -> G instantiations.  G = D when the fragment fits the register
+// budget of the backward, else the largest power of two that does.
+#define SIGB_TRUNC_CASES(X) \
+  X(4, 4, 4)                \
+  X(4, 5, 4)                \
+  X(4, 6, 4)                \
+  X(8, 4, 8)                \
+  X(8, 5, 8)                \
+  X(16, 3, 4)               \
+  X(16, 4, 4)
+
+}  // namespace
+
+bool supported(int64_t d, int depth) {
+#define X(D_, N_, G_) \
+  if (d == D_ && depth == N_) return true;
+  SIGB_TRUNC_CASES(X)
+#undef X
+  return false;
+}
+
+int forward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L, void* out, int64_t out_ld,
+            int64_t out_col0, int include_empty, cudaStream_t stream) {
+#define X(D_, N_, G_)                                                                                      \
+  if (d == D_ && depth == N_) {                                                                            \
+    if (dtype == SIGB_F32)                                                                                 \
+      return fwd<float, D_, N_, G_>((const float*)X, B, L, (float*)out, out_ld, out_col0, include_empty,   \
+                                    stream);                                                               \
+    return fwd<double, D_, N_, G_>((const double*)X, B, L, (double*)out, out_ld, out_col0, include_empty,  \
+                                   stream);                                                                \
+  }
+  SIGB_TRUNC_CASES(X)
+#undef X
+  return fail(SIGB_ERR_UNSUPPORTED, "no truncated kernel for this (d, depth)");
+}
+
+size_t backward_workspace(int dtype, int64_t d, int depth, int64_t B, int64_t L) {
+#define X(D_, N_, G_)                                                                             \
+  if (d == D_ && depth == N_)                                                                     \
+    return dtype == SIGB_F32 ? bwd_workspace<float, D_, N_, G_>(B, L) : bwd_workspace<double, D_, N_, G_>(B, L);
+  SIGB_TRUNC_CASES(X)
+#undef X
+  return 0;
+}
+
+int backward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L, const void* S, int64_t s_ld,
+             int64_t s_col0, const void* g, int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, void* dX,
+             void* dinc, cudaStream_t stream) {
+#define X(D_, N_, G_)                                                                                             \
+  if (d == D_ && depth == N_) {                                                                                   \
+    if (dtype == SIGB_F32)                                                                                        \
+      return bwd<float, D_, N_, G_>((const float*)X, B, L, (const float*)S, s_ld, s_col0, (const float*)g, g_ld,  \
+                                    g_col0, work, work_bytes, (float*)dX, (float*)dinc, stream);                  \
+    return bwd<double, D_, N_, G_>((const double*)X, B, L, (const double*)S, s_ld, s_col0, (const double*)g,     \
+                                   g_ld, g_col0, work, work_bytes, (double*)dX, (double*)dinc, stream);           \
+  }
+  SIGB_TRUNC_CASES(X)
+#undef X
+  return fail(SIGB_ERR_UNSUPPORTED, "no truncated kernel for this (d, depth)");
+}
+
+}  // namespace trunc
+}  // namespace sigb

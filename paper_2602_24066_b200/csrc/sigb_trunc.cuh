@@ -1,0 +1,487 @@
+// Register-resident Chen kernels for fully truncated word sets (all words of
+// length 1..N over D letters): configs 1, 2 and 5 of BASELINE.json.
+//
+// Work decomposition.  A truncated trie is perfectly regular, so each thread
+// owns a fixed FRAGMENT for the whole time sweep, held in registers:
+//   - G sibling "mid" words u_g (length N-1) sharing the grand-parent gp,
+//   - their G*D leaf children u_g∘z (length N),
+//   - the chain of gp's prefixes (lengths 1..N-2), recomputed redundantly by
+//     the Q = D/G threads that share gp (and by every gp below them).
+// One step of Chen's relation in the shared-prefix Horner form (see
+// sigb_level.cu) then costs, per thread,
+//   sum_{k=1}^{N-2} (N-k+1) chain FMAs + 2G mid FMAs + G*D leaf FMAs
+// with no shared memory traffic except the broadcast increments and no
+// barrier inside a chunk of kChunkT steps.  For D=16, N=4, G=4 that is 79
+// FMAs for 68.5 words (the reference executes sum |w|(|w|+1)/2 ~ 680 Horner
+// steps for the same words, _kernels.py:52-57).
+//
+// Backward: the same fragment, with the adjoints lambda.  Leaf adjoints are
+// constant in time (a leaf has a single Horner node), so the reverse step
+// per leaf is two FMAs (adjoint to the parent, gradient).  Per-step
+// gradients dL/d(dX_j) are reduced across the warp by a transposing
+// shuffle butterfly, across warps through shared memory once per chunk, and
+// across the CTAs of a path by sample_grads_kernel, all in fixed order.
+#pragma once
+
+#include "sigb_internal.h"
+
+namespace sigb {
+namespace trunc {
+
+constexpr int kChunkT = 16;  // steps staged per chunk
+constexpr int kThreadsT = 256;
+
+__host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
+
+template <int D, int N, int G>
+struct Cfg {
+  static_assert(N >= 2, "truncated kernel needs depth >= 2");
+  static_assert(D % G == 0, "G must divide D");
+  static constexpr int Q = D / G;                       // threads per grand-parent
+  static constexpr int NC = N - 2;                      // chain length
+  static constexpr int NGP = ipow(D, N - 2);            // grand-parents per path
+  static constexpr int TPP = NGP * Q;                   // threads per path
+  static constexpr int PPC = TPP >= kThreadsT ? 1 : kThreadsT / TPP;  // paths per CTA
+  static constexpr int CPP = TPP >= kThreadsT ? TPP / kThreadsT : 1;  // CTAs per path
+  static constexpr int THREADS = TPP >= kThreadsT ? kThreadsT : PPC * TPP;
+  static constexpr int RW = TPP < 32 ? TPP : 32;        // reduction width (lanes of one path)
+  static constexpr int NW = THREADS / 32 > 0 ? THREADS / 32 : 1;
+  static_assert(TPP % 32 == 0 || 32 % TPP == 0, "threads per path must tile warps");
+  static_assert(D <= (TPP < 32 ? TPP : 32), "letters must not exceed the reduction width");
+  static_assert(TPP < kThreadsT ? kThreadsT % TPP == 0 : TPP % kThreadsT == 0, "CTA tiling");
+  // level offsets in canonical order: O[l] = sum_{k=1}^{l-1} D^k
+  __host__ __device__ static constexpr int64_t off(int l) { return l <= 1 ? 0 : off(l - 1) + ipow(D, l - 1); }
+};
+
+template <typename T, int R>
+__device__ __forceinline__ constexpr T inv() {
+  return T(1) / T(R);
+}
+
+template <typename T>
+__device__ __forceinline__ T shfl_xor(T v, int m) {
+  return __shfl_xor_sync(0xffffffffu, v, m);
+}
+
+// Per-thread fragment geometry.
+template <int D, int N, int G>
+struct Frag {
+  using C = Cfg<D, N, G>;
+  int64_t b;    // path
+  int cip;      // CTA index within the path
+  int t;        // thread index within the path
+  int q;        // which G-slice of gp's children
+  int gp;       // grand-parent code (level N-2)
+  int pc;       // path slot within the CTA
+  int chain_letter[C::NC > 0 ? C::NC : 1];
+
+  __device__ __forceinline__ Frag(int64_t cta, int tid) {
+    if (C::CPP > 1) {
+      b = cta / C::CPP;
+      cip = (int)(cta % C::CPP);
+      t = cip * kThreadsT + tid;
+      pc = 0;
+    } else {
+      pc = tid / C::TPP;
+      b = cta * C::PPC + pc;
+      cip = 0;
+      t = tid % C::TPP;
+    }
+    q = t % C::Q;
+    gp = t / C::Q;
+    int code = gp;
+#pragma unroll
+    for (int k = C::NC - 1; k >= 0; --k) {
+      chain_letter[k] = code % D;
+      code /= D;
+    }
+  }
+  // canonical index of chain node k (length k+1)
+  __device__ __forceinline__ int64_t chain_index(int k) const {
+    return C::off(k + 1) + gp / ipow(D, C::NC - 1 - k);
+  }
+  // this thread emits / seeds chain node k iff it is the first thread below it
+  __device__ __forceinline__ bool chain_owner(int k) const {
+    return q == 0 && gp % ipow(D, C::NC - 1 - k) == 0;
+  }
+  __device__ __forceinline__ int64_t mid_index(int g) const { return C::off(N - 1) + (int64_t)gp * D + q * G + g; }
+  __device__ __forceinline__ int64_t leaf_index(int g, int z) const {
+    return C::off(N) + ((int64_t)gp * D + q * G + g) * D + z;
+  }
+};
+
+// Stage samples of paths of this CTA for steps [j0, j0+cs] and write the
+// increments dX[s][z] (s < cs) to shared memory: layout Dl[pc][s][D].
+template <typename T, int D, int PPC>
+__device__ __forceinline__ void stage_increments(const T* __restrict__ X, int64_t b_first, int64_t B, int64_t L,
+                                                 int j0, int cs, T* __restrict__ Xs, T* __restrict__ Dl) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int rows = cs + 1;
+  for (int i = tid; i < PPC * rows * D; i += nt) {
+    const int pc = i / (rows * D), r = i % (rows * D);
+    const int64_t b = b_first + pc;
+    Xs[pc * (kChunkT + 1) * D + r] = b < B ? X[(b * L + j0) * D + r] : T(0);
+  }
+  __syncthreads();
+  for (int i = tid; i < PPC * cs * D; i += nt) {
+    const int pc = i / (cs * D), r = i % (cs * D);
+    const T* xs = Xs + pc * (kChunkT + 1) * D;
+    Dl[pc * kChunkT * D + r] = xs[r + D] - xs[r];
+  }
+  __syncthreads();
+}
+
+template <typename T, int D>
+__device__ __forceinline__ void load_row(const T* __restrict__ src, T (&v)[D], T sign) {
+  if constexpr (sizeof(T) == 4 && D % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < D; i += 4) {
+      const float4 f = *reinterpret_cast<const float4*>(src + i);
+      v[i] = sign * f.x; v[i + 1] = sign * f.y; v[i + 2] = sign * f.z; v[i + 3] = sign * f.w;
+    }
+  } else if constexpr (sizeof(T) == 8 && D % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < D; i += 2) {
+      const double2 f = *reinterpret_cast<const double2*>(src + i);
+      v[i] = sign * f.x; v[i + 1] = sign * f.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < D; ++i) v[i] = sign * src[i];
+  }
+}
+
+// The thread's fragment state.
+template <typename T, int D, int N, int G>
+struct State {
+  using C = Cfg<D, N, G>;
+  T ch[C::NC > 0 ? C::NC : 1];
+  T mid[G];
+  T leaf[G][D];
+};
+
+// Increments needed by the fragment at one step: all D letters (leaves), the
+// G mid letters and the chain letters.
+template <typename T, int D, int N, int G>
+struct StepIncr {
+  using C = Cfg<D, N, G>;
+  T dz[D];
+  T dy[G];
+  T dc[C::NC > 0 ? C::NC : 1];
+
+  __device__ __forceinline__ void load(const T* __restrict__ row, const Frag<D, N, G>& f, T sign) {
+    load_row<T, D>(row, dz, sign);
+    if constexpr (G == D) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) dy[g] = dz[g];
+    } else {
+#pragma unroll
+      for (int g = 0; g < G; ++g) dy[g] = sign * row[f.q * G + g];
+    }
+#pragma unroll
+    for (int k = 0; k < C::NC; ++k) dc[k] = sign * row[f.chain_letter[k]];
+  }
+};
+
+// Forward partials of the chain: tch[k][m] = T(chain_k, m) for m = k+1..N.
+template <typename T, int D, int N, int G>
+__device__ __forceinline__ void chain_partials(const State<T, D, N, G>& st, const StepIncr<T, D, N, G>& in,
+                                               T (&tch)[Cfg<D, N, G>::NC > 0 ? Cfg<D, N, G>::NC : 1][N + 1]) {
+  constexpr int NC = Cfg<D, N, G>::NC;
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    const int lv = k + 1;
+#pragma unroll
+    for (int m = lv; m <= N; ++m) {
+      const T a = in.dc[k] * (T(1) / T(m - lv + 1));
+      tch[k][m] = (k == 0) ? st.ch[k] + a : fma(a, tch[k > 0 ? k - 1 : 0][m], st.ch[k]);
+    }
+  }
+}
+
+// One forward Chen step S <- S ⊗ exp(dX) on the fragment (in.* already signed).
+template <typename T, int D, int N, int G>
+__device__ __forceinline__ void chen_step(State<T, D, N, G>& st, const StepIncr<T, D, N, G>& in) {
+  constexpr int NC = Cfg<D, N, G>::NC;
+  T tch[NC > 0 ? NC : 1][N + 1];
+  chain_partials<T, D, N, G>(st, in, tch);
+  const T tN1 = NC > 0 ? tch[NC > 0 ? NC - 1 : 0][N - 1] : T(1);
+  const T tN = NC > 0 ? tch[NC > 0 ? NC - 1 : 0][N] : T(1);
+#pragma unroll
+  for (int k = 0; k < NC; ++k) st.ch[k] = tch[k][k + 1];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const T tm = fma(in.dy[g] * inv<T, 2>(), tN, st.mid[g]);  // T(u_g, N)
+    st.mid[g] = fma(in.dy[g], tN1, st.mid[g]);
+#pragma unroll
+    for (int z = 0; z < D; ++z) st.leaf[g][z] = fma(in.dz[z], tm, st.leaf[g][z]);
+  }
+}
+
+template <typename T, int D, int N, int G>
+__global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
+    trunc_forward_kernel(const T* __restrict__ X, int64_t B, int64_t L, T* __restrict__ out, int64_t out_ld,
+                         int64_t out_col0, int include_empty) {
+  using C = Cfg<D, N, G>;
+  __shared__ __align__(16) T Xs[C::PPC * (kChunkT + 1) * D];
+  __shared__ __align__(16) T Dl[C::PPC * kChunkT * D];
+  const Frag<D, N, G> f(blockIdx.x, threadIdx.x);
+  const int64_t b_first = C::CPP > 1 ? f.b : (int64_t)blockIdx.x * C::PPC;
+  State<T, D, N, G> st;
+#pragma unroll
+  for (int k = 0; k < C::NC; ++k) st.ch[k] = T(0);
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    st.mid[g] = T(0);
+#pragma unroll
+    for (int z = 0; z < D; ++z) st.leaf[g][z] = T(0);
+  }
+  const int64_t M = L - 1;
+  for (int64_t j0 = 0; j0 < M; j0 += kChunkT) {
+    const int cs = (int)(M - j0 < kChunkT ? M - j0 : kChunkT);
+    stage_increments<T, D, C::PPC>(X, b_first, B, L, (int)j0, cs, Xs, Dl);
+    const T* rows = Dl + f.pc * kChunkT * D;
+#pragma unroll 1
+    for (int s = 0; s < cs; ++s) {
+      StepIncr<T, D, N, G> in;
+      in.load(rows + s * D, f, T(1));
+      chen_step<T, D, N, G>(st, in);
+    }
+  }
+  if (f.b >= B) return;
+  T* orow = out + f.b * out_ld + out_col0;
+#pragma unroll
+  for (int k = 0; k < C::NC; ++k)
+    if (f.chain_owner(k)) orow[f.chain_index(k)] = st.ch[k];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    orow[f.mid_index(g)] = st.mid[g];
+#pragma unroll
+    for (int z = 0; z < D; ++z) orow[f.leaf_index(g, z)] = st.leaf[g][z];
+  }
+  if (include_empty && f.t == 0) orow[-1] = T(1);
+}
+
+// Transposing butterfly: V values over the WIDTH lanes of each aligned group.
+// On return v[0] holds the group sum of value index `idx` (returned); lanes
+// that differ only in the plain-sum bits hold the same index.
+template <typename T, int V, int WIDTH>
+__device__ __forceinline__ int transpose_reduce(T (&v)[V], int lane) {
+  int idx = 0;
+  int cnt = V;
+#pragma unroll
+  for (int mask = WIDTH / 2; mask >= 1; mask /= 2) {
+    if (cnt > 1) {
+      const int half = cnt / 2;
+      const bool upper = (lane & mask) != 0;
+#pragma unroll
+      for (int i = 0; i < V / 2; ++i) {
+        if (i < half) {
+          const T send = upper ? v[i] : v[i + half];
+          const T keep = upper ? v[i + half] : v[i];
+          v[i] = keep + shfl_xor(send, mask);
+        }
+      }
+      if (upper) idx += half;
+      cnt = half;
+    } else {
+      v[0] += shfl_xor(v[0], mask);
+    }
+  }
+  // V > WIDTH: remaining values stay in v[0..cnt) (not used by the configs here)
+  return idx;
+}
+
+template <int D, int N, int G>
+struct RedGeom {
+  using C = Cfg<D, N, G>;
+  static constexpr int GPW = C::RW / C::Q > 0 ? C::RW / C::Q : 1;  // gp groups per reduction group
+  static constexpr int RGW = 32 / C::RW;                              // reduction groups per warp
+  template <typename T>
+  static constexpr size_t smem_bytes() {
+    return sizeof(T) * ((size_t)C::PPC * (kChunkT + 1) * D + (size_t)C::PPC * kChunkT * D +
+                        (size_t)C::NW * RGW * kChunkT * D + (size_t)C::NW * RGW * kChunkT * GPW * (C::NC > 0 ? C::NC : 1));
+  }
+};
+
+// Backward.  grid: one CTA per (CTA-part of a path) -- paths [b0, b0 + nb).
+// partial layout: [(b - b0) * CPP + cip][M][D].
+template <typename T, int D, int N, int G>
+__global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
+    trunc_backward_kernel(const T* __restrict__ X, int64_t B, int64_t L, int64_t b0, const T* __restrict__ Sin,
+                          int64_t s_ld, int64_t s_col0, const T* __restrict__ gup, int64_t g_ld, int64_t g_col0,
+                          T* __restrict__ partial) {
+  using C = Cfg<D, N, G>;
+  using RG = RedGeom<D, N, G>;
+  constexpr int NC = C::NC;
+  constexpr int NCc = NC > 0 ? NC : 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Xs = reinterpret_cast<T*>(smem_raw);
+  T* Dl = Xs + C::PPC * (kChunkT + 1) * D;
+  // per-warp per-step reduced gradients: leaf/mid letters, and chain terms per gp group
+  T(*red_leaf)[RG::RGW][kChunkT][D] = reinterpret_cast<T(*)[RG::RGW][kChunkT][D]>(Dl + C::PPC * kChunkT * D);
+  T(*red_chain)[RG::RGW][kChunkT][RG::GPW][NCc] =
+      reinterpret_cast<T(*)[RG::RGW][kChunkT][RG::GPW][NCc]>(Dl + C::PPC * kChunkT * D + C::NW * RG::RGW * kChunkT * D);
+  const int64_t cta = blockIdx.x + (C::CPP > 1 ? b0 * C::CPP : b0 / C::PPC);
+  const Frag<D, N, G> f(cta, threadIdx.x);
+  const int64_t b_first = C::CPP > 1 ? f.b : cta * C::PPC;
+  const int64_t M = L - 1;
+  const bool live = f.b < B;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rg = lane / C::RW;  // reduction group inside the warp
+  State<T, D, N, G> st, lam;
+  // terminal state and adjoint seeds
+  {
+    const T* srow = Sin + (live ? f.b : 0) * s_ld + s_col0;
+    const T* grow = gup + (live ? f.b : 0) * g_ld + g_col0;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      st.ch[k] = live ? srow[f.chain_index(k)] : T(0);
+      lam.ch[k] = (live && f.chain_owner(k)) ? grow[f.chain_index(k)] : T(0);
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      st.mid[g] = live ? srow[f.mid_index(g)] : T(0);
+      lam.mid[g] = live ? grow[f.mid_index(g)] : T(0);
+#pragma unroll
+      for (int z = 0; z < D; ++z) {
+        st.leaf[g][z] = live ? srow[f.leaf_index(g, z)] : T(0);
+        lam.leaf[g][z] = live ? grow[f.leaf_index(g, z)] : T(0);
+      }
+    }
+  }
+  const int nchunks = (int)((M + kChunkT - 1) / kChunkT);
+  for (int c = nchunks - 1; c >= 0; --c) {
+    const int j0 = c * kChunkT;
+    const int cs = (int)(M - j0 < kChunkT ? M - j0 : kChunkT);
+    stage_increments<T, D, C::PPC>(X, b_first, B, L, j0, cs, Xs, Dl);
+    const T* rows = Dl + f.pc * kChunkT * D;
+#pragma unroll 1
+    for (int s = cs - 1; s >= 0; --s) {
+      StepIncr<T, D, N, G> in;
+      // (a) rebuild S_{0,t_j} = S_{0,t_{j+1}} ⊗ exp(-dX_j)
+      in.load(rows + s * D, f, T(-1));
+      chen_step<T, D, N, G>(st, in);
+      // (b) forward partials from S_{0,t_j}
+#pragma unroll
+      for (int i = 0; i < D; ++i) in.dz[i] = -in.dz[i];
+#pragma unroll
+      for (int g = 0; g < G; ++g) in.dy[g] = -in.dy[g];
+#pragma unroll
+      for (int k = 0; k < NC; ++k) in.dc[k] = -in.dc[k];
+      T tch[NCc][N + 1];
+      chain_partials<T, D, N, G>(st, in, tch);
+      const T tN1 = NC > 0 ? tch[NCc - 1][N - 1] : T(1);
+      const T tN = NC > 0 ? tch[NCc - 1][N] : T(1);
+      // (c) reverse: leaves, mids, chain
+      T gl[D];
+#pragma unroll
+      for (int z = 0; z < D; ++z) gl[z] = T(0);
+      T gm[G];
+      T tbp1 = T(0), tbp2 = T(0);  // Tbar(gp, N-1), Tbar(gp, N) from the mids
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const T tm = fma(in.dy[g] * inv<T, 2>(), tN, st.mid[g]);  // T(u_g, N)
+        T tb0 = T(0), tb1 = T(0);
+#pragma unroll
+        for (int z = 0; z < D; z += 2) {
+          tb0 = fma(in.dz[z], lam.leaf[g][z], tb0);
+          gl[z] = fma(lam.leaf[g][z], tm, gl[z]);
+          if (z + 1 < D) {
+            tb1 = fma(in.dz[z + 1], lam.leaf[g][z + 1], tb1);
+            gl[z + 1] = fma(lam.leaf[g][z + 1], tm, gl[z + 1]);
+          }
+        }
+        const T tb = tb0 + tb1;  // Tbar(u_g, N)
+        const T lm = lam.mid[g];  // Tbar(u_g, N-1)
+        tbp1 = fma(in.dy[g], lm, tbp1);
+        tbp2 = fma(in.dy[g] * inv<T, 2>(), tb, tbp2);
+        gm[g] = fma(lm, tN1, tb * tN * inv<T, 2>());
+        lam.mid[g] = lm + tb;
+      }
+      // mids' gradient terms join the leaf letters
+      if constexpr (G == D) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) gl[g] += gm[g];
+      } else {
+#pragma unroll
+        for (int qq = 0; qq < C::Q; ++qq)
+#pragma unroll
+          for (int g = 0; g < G; ++g) gl[qq * G + g] += (f.q == qq) ? gm[g] : T(0);
+      }
+      // chain, deepest first: tbc[m] = Tbar(node, m) contributed by its child
+      T gch[NCc];
+      {
+        T tbc[N + 1];
+#pragma unroll
+        for (int m = 0; m <= N; ++m) tbc[m] = T(0);
+        tbc[N - 1] = tbp1;
+        tbc[N] = tbp2;
+#pragma unroll
+        for (int k = NC - 1; k >= 0; --k) {
+          const int lv = k + 1;
+          T tbn[N + 1];
+#pragma unroll
+          for (int m = 0; m <= N; ++m) tbn[m] = (m == lv) ? lam.ch[k] : tbc[m];
+          T lsum = tbn[lv];
+          T gs = T(0);
+#pragma unroll
+          for (int m = lv; m <= N; ++m) {
+            if (m > lv) lsum += tbn[m];
+            const T par = (k == 0) ? T(1) : tch[k > 0 ? k - 1 : 0][m];
+            gs = fma(tbn[m] * (T(1) / T(m - lv + 1)), par, gs);
+          }
+          lam.ch[k] = lsum;
+          gch[k] = gs;
+#pragma unroll
+          for (int m = 0; m <= N; ++m)
+            tbc[m] = (m >= lv) ? in.dc[k] * (T(1) / T(m - lv + 1 > 0 ? m - lv + 1 : 1)) * tbn[m] : T(0);
+        }
+      }
+      // (d) reduce within the path's lanes; park per-warp results in shared memory
+      const int idx = transpose_reduce<T, D, C::RW>(gl, lane);
+      constexpr int plain_bits = C::RW / (D < C::RW ? D : C::RW);  // lanes sharing one letter
+      if ((lane % C::RW) % plain_bits == 0 && D <= C::RW) red_leaf[warp][rg][s][idx] = gl[0];
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        T v = gch[k];
+#pragma unroll
+        for (int msk = 1; msk < C::Q; msk *= 2) v += shfl_xor(v, msk);
+        if (f.q == 0) red_chain[warp][rg][s][(lane % C::RW) / C::Q][k] = v;
+      }
+    }
+    __syncthreads();
+    // chunk epilogue: sum warps (and chain terms by letter) -> partial[path-part][j][z]
+    for (int i = threadIdx.x; i < C::PPC * cs * D; i += blockDim.x) {
+      const int pc = i / (cs * D), s = (i / D) % cs, z = i % D;
+      const int64_t b = b_first + pc;
+      if (b >= B) continue;
+      T acc = T(0);
+      // warps / reduction groups belonging to path slot pc
+#pragma unroll 1
+      for (int w = 0; w < C::NW; ++w) {
+#pragma unroll 1
+        for (int r = 0; r < RG::RGW; ++r) {
+          const int first_thread = w * 32 + r * C::RW;
+          if (first_thread / C::TPP != pc && C::CPP == 1) continue;
+          acc += red_leaf[w][r][s][z];
+#pragma unroll 1
+          for (int gg = 0; gg < RG::GPW; ++gg) {
+            const int tt = (C::CPP > 1 ? f.cip * kThreadsT : 0) + (first_thread % C::TPP) + gg * C::Q;
+            int code = tt / C::Q;
+#pragma unroll
+            for (int k = NC - 1; k >= 0; --k) {
+              if (code % D == z) acc += red_chain[w][r][s][gg][k];
+              code /= D;
+            }
+          }
+        }
+      }
+      partial[(((b - b0) * C::CPP + f.cip) * M + j0 + s) * D + z] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace trunc
+}  // namespace sigb

@@ -294,3 +294,62 @@ def test_module_wrapper():
     gr = np.ones((4, len(ws) + 1))
     ref = sk.signature_backward(X.detach().cpu().numpy(), ws, gr).path_grads
     assert ora.rel_err(X.grad.cpu().numpy(), ref) <= 1e-12
+
+
+# -- both kernel families on the truncated configs ------------------------------------------------
+
+
+@pytest.fixture(params=[0, 1], ids=["auto", "generic"])
+def policy(request):
+    from paper_2602_24066_b200 import _lib
+
+    _lib.set_kernel_policy(request.param)
+    yield request.param
+    _lib.set_kernel_policy(0)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c5"])
+def test_truncated_paths_both_kernels(golden_forward, golden_backward, policy, name):
+    ws = build_wordset(name, sk)
+    g = golden_forward
+    out = sk.signature_forward(g[f"{name}/X"], ws).values
+    tol = TOL64 if CONFIGS[name]["dtype"] == np.float64 else TOL32
+    assert ora.rel_err(out, g[f"{name}/S64"]) <= tol
+    gb = golden_backward
+    dX = sk.signature_backward(gb[f"{name}/X"], ws, gb[f"{name}/g"]).path_grads
+    assert ora.rel_err(dX, gb[f"{name}/dX"]) <= TOL64
+    X = torch.from_numpy(gb[f"{name}/X"].astype(np.float32)).cuda().requires_grad_(True)
+    sk.signature(X, ws).backward(torch.from_numpy(gb[f"{name}/g"]).float().cuda())
+    assert ora.rel_err(X.grad.cpu().numpy(), gb[f"{name}/dX"]) <= TOL32
+
+
+@pytest.mark.parametrize("d,N", [(4, 4), (4, 5), (4, 6), (8, 4), (8, 5), (16, 3), (16, 4)])
+def test_truncated_instantiations_vs_oracle(d, N):
+    ws = sk.build_truncated(d, N, include_empty=True)
+    rng = np.random.default_rng(d * 10 + N)
+    B = 5
+    X = brownian(d + N, B, 9, d)
+    out = sk.signature_forward(X, ws).values
+    assert out[:, 0].tolist() == [1.0] * B
+    ref = ora.forward(X, ws.codes, ws.lengths, d)
+    assert ora.rel_err(out[:, 1:], ref) <= TOL64
+    g = rng.standard_normal((B, len(ws) + 1))
+    dX = sk.signature_backward(X, ws, g).path_grads
+    _, dref = ora.backward(X, ws.codes, ws.lengths, d, g[:, 1:])
+    assert ora.rel_err(dX, dref) <= TOL64
+    X32 = torch.from_numpy(X.astype(np.float32)).cuda().requires_grad_(True)
+    S32 = sk.signature(X32, ws)
+    S32.backward(torch.from_numpy(g).float().cuda())
+    assert ora.rel_err(S32.detach().cpu().numpy()[:, 1:], ref) <= TOL32
+    assert ora.rel_err(X32.grad.cpu().numpy(), dref) <= TOL32
+
+
+def test_truncated_batch_tails():
+    # batch sizes that do not fill the paths-per-CTA tiling of the d=4 kernel
+    ws = sk.build_truncated(4, 4)
+    for B in (1, 3, 17, 33):
+        X = brownian(B, B, 20, 4)
+        g = np.random.default_rng(B).standard_normal((B, len(ws)))
+        assert ora.rel_err(sk.signature_forward(X, ws).values, ora.forward(X, ws.codes, ws.lengths, 4)) <= TOL64
+        _, dref = ora.backward(X, ws.codes, ws.lengths, 4, g)
+        assert ora.rel_err(sk.signature_backward(X, ws, g).path_grads, dref) <= TOL64
