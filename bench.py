@@ -1,0 +1,509 @@
+#!/usr/bin/env python
+"""bench.py -- fwd and fwd+bwd signature throughput (paths/s) on 1..8 B200s.
+
+One JSON line on rank 0 (the driver's contract).  A "step" is one pass of the
+hot path over one batch: the forward Chen kernel (S_{0,T} of every word) and
+the memory-lean backward (dL/dX from S_{0,T} and a dense upstream), both
+through the C ABI (include/sigkit_b200.h) on inputs already resident in HBM.
+
+Workload (default): BASELINE.json config 5 -- truncated signature d=16,
+depth 4 (W = 69,904 words), L = 512 samples, fp32, 65,536 paths PER RANK
+(weak scaling: the batch axis shards with no collective).
+``--strong`` shards a fixed 65,536 paths instead; ``--config c2|c3|c4``
+measures another BASELINE config on the same harness.
+
+Extra keys:
+  fwd          forward-only paths/s (the metric's first half)
+  roofline     the dominant kernel (backward Chen kernel) against the FP32
+               FMA pipe: algorithmic flop per launch / CUDA-event duration
+  roofline_fwd the same for the forward Chen kernel
+  e2e          fwd+bwd paths/s through the public autograd API with the
+               paths copied from pinned host memory and dL/dX + the loss
+               read back every step
+  e2e_fwd      forward paths/s through the numpy drop-in signature_forward
+               (host array in, host array out)
+  cpu_baseline the CPU oracle port (oracle/, a restatement of the reference
+               numba kernels) on this host's cores, bounded sample, N=1 only
+  clocks       nvidia-smi SM clocks / throttle reasons sampled during the
+               timed region
+
+``--impl reference`` times the reference algorithm on the host cores instead
+(the oracle port; the reference is a numba package that cannot travel to the
+GPU box) and prints the same line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "fwd and fwd+bwd signature throughput (paths/sec) at 1/2/4/8 B200"
+FP32_LANES_PER_SM = 128
+FP64_LANES_PER_SM = 64
+
+
+def parse_args(argv=None):
+    p = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--config", default="c5", choices=("c1", "c2", "c3", "c4", "c5"))
+    p.add_argument("--batch", type=int, default=0, help="override the per-rank batch (profiling only)")
+    p.add_argument("--strong", action="store_true", help="shard a fixed global batch instead of per-rank batches")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--gather", action="store_true", help="also time the optional NCCL all-gather of S")
+    p.add_argument("--policy", type=int, default=0, help="0 auto kernels, 1 generic trie kernels only")
+    return p.parse_args(argv)
+
+
+# -- helpers ---------------------------------------------------------------------------
+
+
+def load_peaks() -> dict:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f)
+    return {}
+
+
+def fma_peak_tflops(dtype: str, sms: int, peaks: dict) -> tuple[float, str]:
+    """FMA-pipe peak for the roofline.
+
+    MEASURED_PEAKS.json holds copy bandwidth and bf16 GEMM, not the FP32/FP64
+    FMA pipe, so the peak is MEASURED here, on this GPU, by tools/ubench_fma
+    (64 independent FFMA / 32 DFMA chains per thread, 8 CTAs per SM, best of
+    5).  If the binary is missing, fall back to SMs x lanes x 2 flop x the
+    sm_max_mhz of MEASURED_PEAKS.json, and say so.
+    """
+    exe = os.path.join(ROOT, "tools", "ubench_fma")
+    if os.path.exists(exe):
+        try:
+            out = subprocess.run([exe, "--peak"], capture_output=True, text=True, timeout=60).stdout
+            js = json.loads(out.strip().splitlines()[-1])
+            v = js["ffma_tflops" if dtype == "fp32" else "dfma_tflops"]
+            if v > 0:
+                return v, f"measured on this GPU by tools/ubench_fma --peak ({'FFMA' if dtype == 'fp32' else 'DFMA'})"
+        except (OSError, ValueError, KeyError, IndexError, subprocess.TimeoutExpired):
+            pass
+    mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    lanes = FP32_LANES_PER_SM if dtype == "fp32" else FP64_LANES_PER_SM
+    return sms * lanes * 2 * mhz * 1e6 / 1e12, (
+        f"computed (ubench unavailable): {sms} SMs x {lanes} {dtype} FMA lanes x 2 flop x {mhz:.0f} MHz "
+        "(MEASURED_PEAKS.json sm_max_mhz)")
+
+
+def ncu_traffic(kernel: str, config: str) -> tuple[float | None, str | None]:
+    """DRAM bytes per path of `kernel` from the committed ncu summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(path):
+        return None, None
+    with open(path) as f:
+        js = json.load(f)
+    ent = js.get(config, {}).get(kernel)
+    if not ent or not ent.get("paths"):
+        return None, None
+    return (ent["dram_read_bytes"] + ent["dram_write_bytes"]) / ent["paths"], ent.get("source")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, enabled: bool):
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+        if enabled:
+            try:
+                os.makedirs(os.path.dirname(self.path), exist_ok=True)
+                self.fh = open(self.path, "w")
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200"],
+                    stdout=self.fh, stderr=subprocess.DEVNULL)
+            except (OSError, FileNotFoundError):
+                self.proc = None
+
+    def stop(self) -> dict | None:
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.fh.close()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    rows.append((float(parts[1]), float(parts[2]), float(parts[4]), parts[5:9]))
+                except ValueError:
+                    continue
+        if not rows:
+            return None
+        loaded = [r for r in rows if r[2] >= 50.0] or rows
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in loaded for i, v in enumerate(r[3]) if v.lower().startswith("active")})
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(loaded)}
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def workload(name: str):
+    from tests.configs import CONFIGS
+
+    cfg = dict(CONFIGS[name])
+    return cfg
+
+
+def sum_lengths(ws) -> int:
+    return int(np.asarray(ws.lengths).sum())
+
+
+def describe(name: str, cfg: dict, ws) -> str:
+    kind = cfg["kind"]
+    if kind == "truncated":
+        s = f"truncated d={cfg['d']} depth={cfg['depth']}"
+    elif kind == "custom":
+        s = f"prefix-closed custom trie d={cfg['d']} (seeded, tests/golden/c3_words.json)"
+    else:
+        s = f"anisotropic d={cfg['d']} gamma={list(cfg['gamma'])} r={cfg['r']}"
+    dt = "fp64" if cfg["dtype"] == np.float64 else "fp32"
+    return f"{name}: {s}, W={len(ws)}, L={cfg['L']}, {dt}, fwd+bwd"
+
+
+# -- CPU arm (oracle port of the reference numba kernels) ---------------------------------
+
+
+def cpu_sample(name: str, cfg: dict, ws, threads: int, seed: int = 7):
+    """Time the oracle port on a bounded sample of workload `name`.
+
+    Forward on B_f = min(B, 2*threads) paths in the config dtype (the
+    reference's mixed-precision fp32 path); backward on B_b = min(B, threads)
+    paths in fp64 (the reference backward always upcasts, backward.py:166-167).
+    Returns (fwd+bwd paths/s, fwd paths/s, t_f, t_b, B_f, B_b).
+    """
+    from oracle import oracle as ora  # the checker / CPU baseline, never the product
+    from tests.configs import brownian
+
+    ora.set_threads(threads)
+    B_f = min(cfg["B"], 2 * threads)
+    B_b = min(cfg["B"], threads)
+    X = brownian(seed, max(B_f, B_b), cfg["L"], cfg["d"]).astype(cfg["dtype"])
+    g = np.random.default_rng(seed + 100).standard_normal((B_b, len(ws)))
+    ora.forward(X[:1, :3], ws.codes, ws.lengths, cfg["d"])  # load / warm the library
+    t0 = time.perf_counter()
+    ora.forward(X[:B_f], ws.codes, ws.lengths, cfg["d"])
+    t_f = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ora.backward(X[:B_b], ws.codes, ws.lengths, cfg["d"], g)
+    t_b = time.perf_counter() - t0
+    return 1.0 / (t_f / B_f + t_b / B_b), B_f / t_f, t_f, t_b, B_f, B_b
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # rank 0 alone times the CPU reference; no process group is formed
+    import paper_2602_24066_b200 as sk
+    from tests.configs import build_wordset
+
+    cfg = workload(args.config)
+    ws = build_wordset(args.config, sk)
+    threads = cpu_threads()
+    for _ in range(args.warmup):
+        cpu_sample(args.config, cfg, ws, threads)
+    tf = tb = 0.0
+    nf = nb = 0
+    for _ in range(args.steps):
+        _, _, t_f, t_b, B_f, B_b = cpu_sample(args.config, cfg, ws, threads)
+        tf += t_f
+        tb += t_b
+        nf, nb = B_f, B_b
+    value = 1.0 / ((tf / args.steps) / nf + (tb / args.steps) / nb)
+    dt = "f64" if cfg["dtype"] == np.float64 else "f32"
+    sample = (f"per step: forward of {nf} paths ({dt}) + backward of {nb} paths (f64, the reference backward "
+              f"contract) of {args.config}; full length L={cfg['L']}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "paths/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * (tf + tb) / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dt,
+        "data": "synthetic Brownian paths (tests/configs.py brownian)",
+        "config": {"workload": describe(args.config, cfg, ws), "per_rank_batch": cfg["B"]},
+        "fwd": {"value": nf * args.steps / tf, "unit": "paths/s"},
+        "cpu_baseline": {"value": value, "unit": "paths/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "paths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# -- GPU arm --------------------------------------------------------------------------------
+
+
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_24066_b200 as sk
+    from paper_2602_24066_b200 import _lib
+    from tests.configs import build_wordset
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    _lib.set_kernel_policy(args.policy)
+    cfg = workload(args.config)
+    ws = build_wordset(args.config, sk)
+    plan = ws.plan(dev)
+    B = args.batch or (cfg["B"] // world if args.strong else cfg["B"])
+    L, d = cfg["L"], cfg["d"]
+    M = L - 1
+    tdt = torch.float64 if cfg["dtype"] == np.float64 else torch.float32
+    dts = "fp64" if tdt == torch.float64 else "fp32"
+    W = len(ws)
+    sl = sum_lengths(ws)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+
+    # synthetic Brownian paths on [0,1], generated on the device (seed per rank)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1000 * int(args.config[1]) + rank)
+    X = torch.zeros((B, L, d), dtype=tdt, device=dev)
+    for s in range(0, B, 8192):
+        e = min(B, s + 8192)
+        inc = torch.randn((e - s, M, d), generator=gen, dtype=tdt, device=dev) / math.sqrt(max(M, 1))
+        torch.cumsum(inc, dim=1, out=X[s:e, 1:])
+        del inc
+    g = torch.randn((B, W), generator=gen, dtype=tdt, device=dev)
+    S = torch.empty((B, W), dtype=tdt, device=dev)
+    dXo = torch.empty_like(X)
+    work = torch.empty(max(plan.workspace_bytes(tdt, B, L, 0), 1), dtype=torch.uint8, device=dev)
+
+    def step():
+        plan.forward(X, S, 0, False)
+        plan.backward(X, S, 0, False, g, 0, 0, dXo, work=work)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+
+    clocks = ClockSampler(enabled=(local == 0))
+    _lib.timing_enable(True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps + 1)]
+    n0 = _lib.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    ev[0].record()
+    for k in range(args.steps):
+        plan.forward(X, S, 0, False)
+        ev[2 * k + 1].record()
+        plan.backward(X, S, 0, False, g, 0, 0, dXo, work=work)
+        ev[2 * k + 2].record()
+    torch.cuda.synchronize()
+    barrier()
+    launches = _lib.launch_count() - n0
+    clk = clocks.stop()
+    total_ms = ev[0].elapsed_time(ev[-1])
+    fwd_ms = sum((ev[0] if k == 0 else ev[2 * k]).elapsed_time(ev[2 * k + 1]) for k in range(args.steps))
+    kf_ms, kf_n = _lib.timing_read(0)
+    kb_ms, kb_n = _lib.timing_read(1)
+    _lib.timing_enable(False)
+    total_ms = max_over_ranks(total_ms)
+    fwd_ms = max_over_ranks(fwd_ms)
+    kf_ms = max_over_ranks(kf_ms)
+    kb_ms = max_over_ranks(kb_ms)
+    paths_step = B * world
+    ms_per_step = total_ms / args.steps
+    value = paths_step / (ms_per_step / 1e3)
+    fwd_value = paths_step * args.steps / (fwd_ms / 1e3)
+
+    peaks = load_peaks()
+    peak, peak_src = fma_peak_tflops(dts, sms, peaks)
+    f_fwd_path = 2.0 * M * sl  # one multiply-add per (word, split)
+    f_bwd_path = 3.0 * f_fwd_path
+
+    def roof(kname, flop_path, k_ms, k_n, bytes_path):
+        if k_n == 0 or k_ms <= 0:
+            return None
+        achieved = flop_path * B * args.steps / (k_ms / 1e3) / 1e12  # per rank, per launch average
+        tr, src = ncu_traffic(kname, args.config)
+        per_launch_paths = B * args.steps / k_n
+        return {"bound": "fma", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None if tr is None else tr * per_launch_paths,
+                "algorithmic_bytes": bytes_path * per_launch_paths, "flop_per_launch": flop_path * per_launch_paths,
+                "launch_ms": k_ms / k_n, "launches": k_n, "peak_source": peak_src,
+                "traffic_source": src}
+
+    s_el = 8 if tdt == torch.float64 else 4
+    bytes_fwd = (L * d + W) * s_el
+    bytes_bwd = (2 * L * d + 2 * W) * s_el
+    kb_name = "trunc_backward_kernel" if plan.uses_truncated else "backward_kernel"
+    kf_name = "trunc_forward_kernel" if plan.uses_truncated else "forward_kernel"
+    roof_b = roof(kb_name, f_bwd_path, kb_ms, kb_n, bytes_bwd)
+    roof_f = roof(kf_name, f_fwd_path, kf_ms, kf_n, bytes_fwd)
+    dominant = roof_b if (roof_b and kb_ms >= kf_ms) else roof_f
+
+    del work
+    # -- optional all-gather of S (kept out of the headline) -----------
+    gather = None
+    if args.gather and world > 1:
+        Bg = min(B, max(1, (4 << 30) // (W * s_el * world)))
+        src = S[:Bg].contiguous()
+        dst = torch.empty((Bg * world, W), dtype=tdt, device=dev)
+        for _ in range(2):
+            dist.all_gather_into_tensor(dst, src)
+        torch.cuda.synchronize()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(3):
+            dist.all_gather_into_tensor(dst, src)
+        b.record()
+        torch.cuda.synchronize()
+        gms = max_over_ranks(a.elapsed_time(b) / 3)
+        gather = {"paths_per_rank": Bg, "ms": gms, "bytes_received_per_rank": Bg * W * s_el * (world - 1),
+                  "GBps_per_rank": Bg * W * s_el * (world - 1) / (gms / 1e3) / 1e9}
+        del src, dst
+
+    # -- end to end: public API, host buffers --------------------------------------------
+    e2e = e2e_fwd = None
+    if not args.no_e2e:
+        del S, g, dXo
+        torch.cuda.empty_cache()
+        Xh = X.cpu().pin_memory()
+        del X
+        torch.cuda.empty_cache()
+        readout = torch.randn((W,), generator=gen, dtype=tdt, device=dev)
+        dXh = torch.empty_like(Xh).pin_memory()
+        lossh = torch.empty((), dtype=tdt).pin_memory()
+
+        def e2e_step():
+            Xd = Xh.to(dev, non_blocking=True).requires_grad_(True)
+            Sd = sk.signature(Xd, ws)
+            loss = (Sd @ readout).sum()
+            loss.backward()
+            dXh.copy_(Xd.grad, non_blocking=True)
+            lossh.copy_(loss.detach(), non_blocking=True)
+
+        for _ in range(max(1, min(args.warmup, 2))):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            e2e_step()
+        b.record()
+        torch.cuda.synchronize()
+        barrier()
+        ems = max_over_ranks(a.elapsed_time(b)) / args.steps
+        e2e = {"value": paths_step / (ems / 1e3), "unit": "paths/s", "ms_per_step": ems,
+               "h2d_bytes_per_step": int(Xh.numel() * Xh.element_size()),
+               "d2h_bytes_per_step": int(dXh.numel() * dXh.element_size() + lossh.element_size()),
+               "api": "paper_2602_24066_b200.signature (autograd) on pinned host paths; loss = (S @ r).sum(); "
+                      "dL/dX and loss copied back"}
+        # forward through the numpy drop-in (signature_forward: host array in, host array out)
+        Bn = min(B, max(1, (8 << 30) // (W * s_el)))
+        Xn = Xh[:Bn].numpy()
+        del Xh, dXh
+        torch.cuda.empty_cache()
+        sk.signature_forward(Xn, ws)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        reps = max(1, min(args.steps, 3))
+        for _ in range(reps):
+            sk.signature_forward(Xn, ws)
+        torch.cuda.synchronize()
+        fms = max_over_ranks((time.perf_counter() - t0) * 1e3 / reps)
+        e2e_fwd = {"value": Bn * world / (fms / 1e3), "unit": "paths/s", "ms_per_step": fms,
+                   "paths_per_rank": Bn, "h2d_bytes_per_step": int(Xn.nbytes), "d2h_bytes_per_step": Bn * W * s_el,
+                   "api": "signature_forward(numpy) -> CoefficientBatch(numpy); host-synchronous wall clock"}
+
+    # -- CPU baseline (rank 0, N = 1 only) -------------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = cpu_threads()
+        v, vf, t_f, t_b, B_f, B_b = cpu_sample(args.config, cfg, ws, threads)
+        cpu = {"value": v, "unit": "paths/s", "cores": threads, "kind": "port", "fwd_value": vf,
+               "sample": f"oracle port (oracle/sig_oracle.c, OpenMP) of the reference numba kernels: forward of "
+                         f"{B_f} paths ({'f64' if tdt == torch.float64 else 'f32'}) in {t_f:.2f} s + backward of "
+                         f"{B_b} paths (f64, reference contract) in {t_b:.2f} s, full L={L}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "paths/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": dts.replace("fp", "f"),
+            "data": "synthetic Brownian paths on [0,1] (dX ~ N(0, 1/M)), generated on device per rank; "
+                    "dense N(0,1) upstream",
+            "config": {"workload": describe(args.config, cfg, ws), "per_rank_batch": B, "global_batch": B * world,
+                       "length": L, "d": d, "W": W, "sum_word_len": sl,
+                       "parallelism": f"dp{world}: batch-sharded, no collective in fwd/bwd",
+                       "l2": "no flush: every pass streams inputs larger than L2 (X %.2f GB, S %.2f GB per rank)"
+                             % (B * L * d * s_el / 1e9, B * W * s_el / 1e9),
+                       "kernels": "truncated register-resident" if plan.uses_truncated else "generic trie"},
+            "fwd": {"value": fwd_value, "unit": "paths/s", "ms_per_step": fwd_ms / args.steps},
+            "roofline": dominant, "roofline_fwd": roof_f if dominant is not roof_f else roof_b,
+            "cpu_baseline": cpu, "e2e": e2e, "e2e_fwd": e2e_fwd, "gather": gather,
+            "gpu_launches": launches, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main(argv=None) -> None:
+    args = parse_args(argv)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

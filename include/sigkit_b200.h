@@ -57,6 +57,14 @@ int sigb_device_sm_count(void);
 int sigb_set_kernel_policy(int policy);
 /* Number of device kernels this library has launched (process-wide). */
 long long sigb_launch_count(void);
+/* CUDA-event timing of the main Chen kernels, recorded on the launch stream
+ * (bench.py's roofline leg).  sigb_timing_enable(1) resets and arms it;
+ * sigb_timing_read(which, &ms, &n) synchronises on the recorded events and
+ * returns the summed device time and launch count since the last read,
+ * which = 0 forward kernel, 1 backward kernel.  No reference counterpart
+ * (the reference times whole calls with perf_counter, bench.py:25-39). */
+int sigb_timing_enable(int on);
+int sigb_timing_read(int which, double* ms, int64_t* launches);
 
 /*
  * Word-set tables on device.  Replaces WordSet.letters (wordsets.py:176-188),
@@ -95,6 +103,10 @@ int64_t sigb_plan_closure_size(const sigb_plan* plan);
 int64_t sigb_plan_num_parts(const sigb_plan* plan);
 /* Executed FMA count of one Chen step of one path (T-node count; diagnostics). */
 int64_t sigb_plan_step_fmas(const sigb_plan* plan);
+/* Kernel family sigb_forward / sigb_backward will run for this plan under the
+ * current policy: 1 = register-resident truncated kernels, 0 = generic trie
+ * kernels, -1 = NULL plan. */
+int sigb_plan_kernel_kind(const sigb_plan* plan);
 
 /*
  * Forward signature.  Replaces forward_kernel (_kernels.py:40-58) together

@@ -37,12 +37,15 @@ SIGNATURES = {
     "sigb_device_sm_count": (ctypes.c_int, []),
     "sigb_set_kernel_policy": (_C, [_C]),
     "sigb_launch_count": (ctypes.c_longlong, []),
+    "sigb_timing_enable": (_C, [_C]),
+    "sigb_timing_read": (_C, [_C, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I)]),
     "sigb_wordset_tables": (_C, [_P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     "sigb_plan_create": (_C, [_P, _P, _I, _I, ctypes.POINTER(_P), _P]),
     "sigb_plan_destroy": (_C, [_P]),
     "sigb_plan_closure_size": (_I, [_P]),
     "sigb_plan_num_parts": (_I, [_P]),
     "sigb_plan_step_fmas": (_I, [_P]),
+    "sigb_plan_kernel_kind": (_C, [_P]),
     "sigb_forward": (_C, [_P, _C, _P, _I, _I, _P, _I, _I, _C, _P, _P]),
     "sigb_windows": (_C, [_P, _C, _P, _I, _I, _P, _I, _P, _P]),
     "sigb_backward_workspace_size": (_C, [_P, _C, _I, _I, _I, ctypes.POINTER(ctypes.c_size_t)]),
@@ -88,3 +91,16 @@ def set_kernel_policy(policy: int) -> None:
 
 def launch_count() -> int:
     return int(lib().sigb_launch_count())
+
+
+def timing_enable(on: bool = True) -> None:
+    """Arm (and reset) CUDA-event timing of the main Chen kernels."""
+    check(lib().sigb_timing_enable(int(on)))
+
+
+def timing_read(which: int) -> tuple[float, int]:
+    """(device ms, launches) of the forward (0) / backward (1) kernel since the last read."""
+    ms = ctypes.c_double()
+    n = ctypes.c_int64()
+    check(lib().sigb_timing_read(int(which), ctypes.byref(ms), ctypes.byref(n)))
+    return float(ms.value), int(n.value)

@@ -51,5 +51,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
+def build_ubench(force: bool = False) -> str:
+    """tools/ubench_fma: the FFMA/DFMA pipe microbenchmark bench.py uses for the roofline peak."""
+    root = os.path.dirname(HERE)
+    src = os.path.join(root, "tools", "ubench_fma.cu")
+    out = os.path.join(root, "tools", "ubench_fma")
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(src):
+        return out
+    subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-o", out, src], check=True,
+                   capture_output=True)
+    return out
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))

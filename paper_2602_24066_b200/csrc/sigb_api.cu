@@ -14,6 +14,35 @@ int g_policy = 0;
 static std::atomic<long long> g_launches{0};
 void count_launch(int n) { g_launches += n; }
 
+// -- optional event timing of the main kernels ---------------------------------------
+namespace {
+struct TimerSlot {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;  // one pair per launch since the last reset
+  size_t used = 0;
+};
+bool g_timing = false;
+TimerSlot g_slots[2];
+}  // namespace
+
+void timing_begin(int which, cudaStream_t stream) {
+  if (!g_timing) return;
+  TimerSlot& t = g_slots[which];
+  if (t.used == t.ev.size()) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    t.ev.emplace_back(a, b);
+  }
+  cudaEventRecord(t.ev[t.used].first, stream);
+}
+
+void timing_end(int which, cudaStream_t stream) {
+  if (!g_timing) return;
+  TimerSlot& t = g_slots[which];
+  cudaEventRecord(t.ev[t.used].second, stream);
+  ++t.used;
+}
+
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
@@ -61,9 +90,11 @@ int forward_t(const sigb_plan* p, const void* X, int64_t B, int64_t L, const int
   const int64_t grid = B * K * p->num_parts;
   if (grid == 0) return SIGB_OK;
   count_launch();
+  if (!ckpt) timing_begin(0, stream);
   forward_kernel<T><<<(unsigned)grid, kThreads, smem, stream>>>(
       p->dev(), (const T*)X, L, bounds, K, (T*)out, out_ld, out_col0, include_empty, (T*)state, p->Wc, ckpt,
       stride, nck, p->max_n);
+  if (!ckpt) timing_end(0, stream);
   SIGB_CUDA_TRY(cudaGetLastError());
   return SIGB_OK;
 }
@@ -114,9 +145,11 @@ int backward_t(const sigb_plan* p, const void* X, int64_t B, int64_t L, const vo
       if (rc) return rc;
     }
     count_launch(2);
+    timing_begin(1, stream);
     backward_kernel<T><<<(unsigned)(Bc * p->num_parts), kThreads, smem, stream>>>(
         p->dev(), (const T*)X, L, b0, (const T*)S, s_ld, s_col0, s_is_state, p->Wc, (const T*)g, g_ld, g_col0,
         ckpt, stride, geo.nck, p->max_n, partial);
+    timing_end(1, stream);
     SIGB_CUDA_TRY(cudaGetLastError());
     const int64_t n = Bc * L * p->d;
     sample_grads_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(partial, Bc, p->num_parts, M, p->d, b0,
@@ -142,12 +175,35 @@ int check_common(const sigb_plan* p, int dtype, int64_t B, int64_t L) {
 using namespace sigb;
 
 extern "C" int sigb_version(void) { return 100; }
+extern "C" int sigb_plan_kernel_kind(const sigb_plan* plan) { return plan ? (use_trunc(plan) ? 1 : 0) : -1; }
 extern "C" int sigb_set_kernel_policy(int policy) {
   if (policy < 0 || policy > 1) return fail(SIGB_ERR_DOMAIN, "kernel policy must be 0 (auto) or 1 (generic)");
   g_policy = policy;
   return SIGB_OK;
 }
 extern "C" long long sigb_launch_count(void) { return g_launches.load(); }
+
+extern "C" int sigb_timing_enable(int on) {
+  g_timing = on != 0;
+  for (TimerSlot& t : g_slots) t.used = 0;
+  return SIGB_OK;
+}
+
+extern "C" int sigb_timing_read(int which, double* ms, int64_t* launches) {
+  if (which < 0 || which > 1 || !ms) return fail(SIGB_ERR_DOMAIN, "timing slot must be 0 (forward) or 1 (backward)");
+  TimerSlot& t = g_slots[which];
+  double total = 0;
+  for (size_t i = 0; i < t.used; ++i) {
+    SIGB_CUDA_TRY(cudaEventSynchronize(t.ev[i].second));
+    float x = 0;
+    SIGB_CUDA_TRY(cudaEventElapsedTime(&x, t.ev[i].first, t.ev[i].second));
+    total += x;
+  }
+  *ms = total;
+  if (launches) *launches = (int64_t)t.used;
+  t.used = 0;
+  return SIGB_OK;
+}
 extern "C" const char* sigb_last_error(void) { return g_last_error.c_str(); }
 
 extern "C" int sigb_device_sm_count(void) {
@@ -170,7 +226,6 @@ extern "C" int sigb_forward(const sigb_plan* plan, int dtype, const void* d_X, i
   if (rc) return rc;
   if (include_empty && out_col0 < 1) return fail(SIGB_ERR_SHAPE, "include_empty needs out_col0 >= 1");
   if (use_trunc(plan)) {
-    count_launch();
     return trunc::forward(dtype, plan->d, plan->trunc_depth, d_X, B, L, d_out, out_ld, out_col0, include_empty,
                           (cudaStream_t)stream);
   }
@@ -224,7 +279,6 @@ extern "C" int sigb_backward(const sigb_plan* plan, int dtype, const void* d_X, 
     return fail(SIGB_ERR_DOMAIN, "word set is not prefix-closed: pass the closure state from sigb_forward");
   if (use_trunc(plan) && ckpt_stride == 0 && B > 0 && L > 1) {
     if (s_is_state) { s_ld = plan->Wc; s_col0 = 0; }
-    count_launch(2);
     return trunc::backward(dtype, plan->d, plan->trunc_depth, d_X, B, L, d_S, s_ld, s_col0, d_g, g_ld, g_col0, d_work,
                            work_bytes, d_dX, d_dinc, (cudaStream_t)stream);
   }

@@ -94,6 +94,10 @@ namespace sigb {
 // kernel-routing policy (sigb_set_kernel_policy) and launch counter
 extern int g_policy;
 void count_launch(int n = 1);
+// Optional CUDA-event timing of the main kernels (sigb_timing_enable):
+// `which` 0 = forward Chen kernel, 1 = backward Chen kernel (summed over batch chunks).
+void timing_begin(int which, cudaStream_t stream);
+void timing_end(int which, cudaStream_t stream);
 namespace trunc {
 bool supported(int64_t d, int depth);
 int forward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L, void* out, int64_t out_ld,

@@ -17,8 +17,11 @@ int fwd(const T* X, int64_t B, int64_t L, T* out, int64_t out_ld, int64_t out_co
   const int64_t grid = C::CPP > 1 ? B * C::CPP : (B + C::PPC - 1) / C::PPC;
   if (grid == 0) return SIGB_OK;
   constexpr size_t smem = sizeof(T) * ((size_t)C::PPC * (kChunkT + 1) * D + (size_t)C::PPC * kChunkT * D);
+  count_launch();
+  timing_begin(0, stream);
   trunc_forward_kernel<T, D, N, G><<<(unsigned)grid, C::THREADS, smem, stream>>>(X, B, L, out, out_ld, out_col0,
                                                                                 include_empty);
+  timing_end(0, stream);
   SIGB_CUDA_TRY(cudaGetLastError());
   return SIGB_OK;
 }
@@ -77,8 +80,11 @@ int bwd(const T* X, int64_t B, int64_t L, const T* S, int64_t s_ld, int64_t s_co
   for (int64_t b0 = 0; b0 < B; b0 += chunk) {
     const int64_t Bc = std::min(chunk, B - b0);
     const int64_t grid = C::CPP > 1 ? Bc * C::CPP : (Bc + C::PPC - 1) / C::PPC;
+    count_launch(2);
+    timing_begin(1, stream);
     trunc_backward_kernel<T, D, N, G><<<(unsigned)grid, C::THREADS, smem, stream>>>(
         X, B, L, b0, S, s_ld, s_col0, g, g_ld, g_col0, partial);
+    timing_end(1, stream);
     SIGB_CUDA_TRY(cudaGetLastError());
     const int64_t n = Bc * L * D;
     trunc_sample_grads<T><<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(partial, Bc, C::CPP, M, D, b0, B, dX,

@@ -95,6 +95,11 @@ class Plan:
         self.step_fmas = int(L.sigb_plan_step_fmas(h))
         self.prefix_closed = self.Wc == self.W
 
+    @property
+    def uses_truncated(self) -> bool:
+        """True when the register-resident truncated kernels serve this plan (current policy)."""
+        return int(_lib.lib().sigb_plan_kernel_kind(self.handle)) == 1
+
     def __del__(self):
         h = getattr(self, "handle", None)
         if h is not None and h.value:
@@ -126,10 +131,12 @@ class Plan:
         return int(n.value)
 
     def backward(self, X: torch.Tensor, S: torch.Tensor, s_col0: int, s_is_state: bool, g: torch.Tensor,
-                 g_col0: int, stride: int, dX: torch.Tensor, dinc: torch.Tensor | None = None) -> None:
+                 g_col0: int, stride: int, dX: torch.Tensor, dinc: torch.Tensor | None = None,
+                 work: torch.Tensor | None = None) -> None:
         B, L, _ = X.shape
         nbytes = self.workspace_bytes(X.dtype, B, L, stride)
-        work = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.device)
+        if work is None or work.numel() < nbytes:
+            work = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.device)
         _lib.check(_lib.lib().sigb_backward(self.handle, dtype_code(X.dtype), ptr(X), B, L, ptr(S), S.shape[1],
                                             s_col0, int(s_is_state), ptr(g), g.shape[1], g_col0, stride,
                                             ptr(work), nbytes, ptr(dX), ptr(dinc), stream_ptr(self.device)))
