@@ -6,8 +6,8 @@
  * compiled code at exactly three call sites, all numba kernels that receive
  * caller-allocated C-contiguous arrays and return nothing:
  *
- *   sigcore.py:421   _kernels.forward_kernel(incr, letters, lengths, inv, out)
- *   sigcore.py:441   _kernels.windows_kernel(incr, letters, lengths, bounds, inv, out)
+ *   sigcore.py:238   _kernels.forward_kernel(incr, letters, lengths, inv, out)
+ *   sigcore.py:258   _kernels.windows_kernel(incr, letters, lengths, bounds, inv, out)
  *   backward.py:203  _kernels.backward_kernel(incr, letters, lengths, upstream, inv,
  *                                            stride, left, right, dh, acc, ckpt, inc_grads)
  *
@@ -110,8 +110,8 @@ int sigb_plan_kernel_kind(const sigb_plan* plan);
 
 /*
  * Forward signature.  Replaces forward_kernel (_kernels.py:40-58) together
- * with the increments (sigcore.py:263-271, fused: the kernel differences the
- * samples itself) and the epsilon column (sigcore.py:401-407).
+ * with the increments (sigcore.py:80-88, fused: the kernel differences the
+ * samples itself) and the epsilon column (sigcore.py:218-224).
  *   d_X      (B, L, d) samples, dtype
  *   d_out    row b at d_out + b*out_ld; word k of I is written at column out_col0+k;
  *            if include_empty, column out_col0-1 is set to 1 (needs out_col0 >= 1)
@@ -126,7 +126,7 @@ int sigb_forward(const sigb_plan* plan, int dtype, const void* d_X, int64_t B, i
 /*
  * Windowed signatures.  Replaces windows_kernel (_kernels.py:61-82):
  * d_bounds int64 (K, 2) sample-index pairs 0 <= l < r <= L-1 (validated by
- * the caller, sigcore.py:321-346); d_out (B, K, W) -- window k of path b
+ * the caller, sigcore.py:138-163); d_out (B, K, W) -- window k of path b
  * at d_out + (b*K + k)*W.
  */
 int sigb_windows(const sigb_plan* plan, int dtype, const void* d_X, int64_t B, int64_t L,

@@ -7,10 +7,10 @@
  *
  * Every routine restates one reference routine (paths relative to
  * /root/reference/pkg/src/sigkit):
- *   ora_increments        sigcore.py:263-271   PathBatch.increments
+ *   ora_increments        sigcore.py:80-88   PathBatch.increments
  *   ora_letters           wordsets.py:176-188  WordSet.letters
  *   ora_factor_table      wordsets.py:205-228  WordSet._factor_table (prefix/suffix)
- *   ora_forward_{f32,f64} _kernels.py:40-58    forward_kernel  (+ sigcore.py:384-389 inv)
+ *   ora_forward_{f32,f64} _kernels.py:40-58    forward_kernel  (+ sigcore.py:201-206 inv)
  *   ora_windows_{f32,f64} _kernels.py:61-82    windows_kernel
  *   ora_backward_f64      _kernels.py:85-183   backward_kernel (+ backward.py:186-200 buffers)
  *   ora_sample_grads      backward.py:130-147  increment_to_sample_grads
@@ -36,7 +36,7 @@ static uint64_t upow(uint64_t d, int64_t e) {
   return p;
 }
 
-/* sigcore.py:263-271 -- per-path X[1:] - X[:-1] in the sample dtype. */
+/* sigcore.py:80-88 -- per-path X[1:] - X[:-1] in the sample dtype. */
 void ora_increments_f64(const double* X, int64_t B, int64_t L, int64_t d, double* out) {
   int64_t M = L - 1;
   for (int64_t b = 0; b < B; ++b)
@@ -98,7 +98,7 @@ void ora_factor_table(const uint64_t* codes, const int64_t* lengths, int64_t W, 
   }
 }
 
-/* _kernels.py:40-58 with sigcore.py:384-389 (inv in the path dtype). */
+/* _kernels.py:40-58 with sigcore.py:201-206 (inv in the path dtype). */
 void ora_forward_f64(const double* incr, int64_t B, int64_t M, int64_t d, const int64_t* letters,
                      const int64_t* lengths, int64_t W, int64_t max_len, double* out) {
   double* inv = (double*)calloc((size_t)max_len + 1, sizeof(double));

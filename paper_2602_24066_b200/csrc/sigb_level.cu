@@ -4,7 +4,7 @@
 // One CTA owns one (path, part).  The part's signature state S lives in
 // shared memory for the whole time sweep; increments are staged kChunk steps
 // at a time, already multiplied by inv[r] = 1/r (the reference's `inv` table,
-// sigcore.py:384-389).
+// sigcore.py:201-206).
 //
 // Forward step (Chen's relation in Horner form, Alg. 1).
 // The reference recomputes, for every word, the Horner chain of every prefix

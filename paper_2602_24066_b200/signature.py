@@ -207,7 +207,7 @@ def forward_tensor(X: torch.Tensor, ws: WordSet, want_state: bool = False):
 
 
 def signature_forward(paths, ws: WordSet, threads: int | None = None) -> CoefficientBatch:
-    """Signature coefficients of each path at every word of the set (sigcore.py:410-422).
+    """Signature coefficients of each path at every word of the set (sigcore.py:227-239).
 
     ``threads`` is accepted for API compatibility; the GPU grid is fixed by the plan.
     """
@@ -225,7 +225,7 @@ def signature_forward(paths, ws: WordSet, threads: int | None = None) -> Coeffic
 
 
 def signature_windows(paths, ws: WordSet, windows, threads: int | None = None) -> list[CoefficientBatch]:
-    """Independent signatures of K sample windows (sigcore.py:425-446)."""
+    """Independent signatures of K sample windows (sigcore.py:242-263)."""
     paths = as_path_batch(paths)
     _check_compute(paths, ws)
     if not isinstance(windows, WindowSpec):

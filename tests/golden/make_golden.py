@@ -107,7 +107,7 @@ def main():
 
     # -- forward ------------------------------------------------------------------
     fwd = {}
-    # known-answer tests from the reference suite (test_sigcore.py:80-111)
+    # known-answer tests from the reference suite (test_sigcore.py:80-88)
     fwd["kat_segment/X"] = np.array([[[0.0, 0.0], [1.0, 2.0]]])
     fwd["kat_segment/S"] = sigkit.signature_forward(fwd["kat_segment/X"], sigkit.build_truncated(2, 2)).values
     fwd["kat_lpath/X"] = np.array([[[0.0, 0.0], [1.0, 0.0], [1.0, 1.0]]])
