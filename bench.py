@@ -299,7 +299,15 @@ def run_ours(args) -> None:
     cfg = workload(args.config)
     ws = build_wordset(args.config, sk)
     plan = ws.plan(dev)
-    B = args.batch or (cfg["B"] // world if args.strong else cfg["B"])
+    from paper_2602_24066_b200.sharding import shard_range
+
+    if args.batch:
+        B = args.batch
+    elif args.strong:  # a fixed global batch, contiguous balanced shards (sharding.shard_range)
+        lo, hi = shard_range(cfg["B"], rank, world)
+        B = hi - lo
+    else:  # weak scaling: every rank runs the config's batch
+        B = cfg["B"]
     L, d = cfg["L"], cfg["d"]
     M = L - 1
     tdt = torch.float64 if cfg["dtype"] == np.float64 else torch.float32
@@ -356,7 +364,7 @@ def run_ours(args) -> None:
     fwd_ms = max_over_ranks(fwd_ms)
     kf_ms = max_over_ranks(kf_ms)
     kb_ms = max_over_ranks(kb_ms)
-    paths_step = B * world
+    paths_step = cfg["B"] if (args.strong and not args.batch) else B * world
     ms_per_step = total_ms / args.steps
     value = paths_step / (ms_per_step / 1e3)
     fwd_value = paths_step * args.steps / (fwd_ms / 1e3)
@@ -481,7 +489,7 @@ def run_ours(args) -> None:
             "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": dts.replace("fp", "f"),
             "data": "synthetic Brownian paths on [0,1] (dX ~ N(0, 1/M)), generated on device per rank; "
                     "dense N(0,1) upstream",
-            "config": {"workload": describe(args.config, cfg, ws), "per_rank_batch": B, "global_batch": B * world,
+            "config": {"workload": describe(args.config, cfg, ws), "per_rank_batch": B, "global_batch": paths_step,
                        "length": L, "d": d, "W": W, "sum_word_len": sl,
                        "parallelism": f"dp{world}: batch-sharded, no collective in fwd/bwd",
                        "l2": "no flush: every pass streams inputs larger than L2 (X %.2f GB, S %.2f GB per rank)"
