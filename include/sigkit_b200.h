@@ -52,7 +52,8 @@ const char* sigb_last_error(void);
 /* Number of SMs of the current device (grid sizing helper). */
 int sigb_device_sm_count(void);
 /* Kernel routing: 0 = auto (register-resident truncated kernels where an
- * instantiation exists, generic trie kernels otherwise), 1 = generic only.
+ * instantiation exists, else fragment kernels, else level kernels),
+ * 1 = level kernels only, 2 = fragment kernels (then level kernels).
  * Process-wide; used by the tests to check both paths against the oracle. */
 int sigb_set_kernel_policy(int policy);
 /* Number of device kernels this library has launched (process-wide). */
@@ -104,9 +105,14 @@ int64_t sigb_plan_num_parts(const sigb_plan* plan);
 /* Executed FMA count of one Chen step of one path (T-node count; diagnostics). */
 int64_t sigb_plan_step_fmas(const sigb_plan* plan);
 /* Kernel family sigb_forward / sigb_backward will run for this plan under the
- * current policy: 1 = register-resident truncated kernels, 0 = generic trie
- * kernels, -1 = NULL plan. */
+ * current policy: 1 = register-resident truncated kernels, 2 = register-resident
+ * fragment kernels (any trie), 0 = level-synchronous trie kernels, -1 = NULL plan. */
 int sigb_plan_kernel_kind(const sigb_plan* plan);
+/* Host-only (no device): the fragment decomposition the plan would use for
+ * this word set.  info[8] = {NC, G, K, fragments, CTAs per path, |cl(I)|,
+ * estimated issue slots per path-step, instantiated (0/1)}.  Fails with
+ * SIGB_ERR_UNSUPPORTED when no fragment shape fits. */
+int sigb_fragment_plan_info(const uint64_t* codes, const int64_t* lengths, int64_t W, int64_t d, int64_t* info);
 
 /*
  * Forward signature.  Replaces forward_kernel (_kernels.py:40-58) together

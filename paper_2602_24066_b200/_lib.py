@@ -46,6 +46,7 @@ SIGNATURES = {
     "sigb_plan_num_parts": (_I, [_P]),
     "sigb_plan_step_fmas": (_I, [_P]),
     "sigb_plan_kernel_kind": (_C, [_P]),
+    "sigb_fragment_plan_info": (_C, [_P, _P, _I, _I, _P]),
     "sigb_forward": (_C, [_P, _C, _P, _I, _I, _P, _I, _I, _C, _P, _P]),
     "sigb_windows": (_C, [_P, _C, _P, _I, _I, _P, _I, _P, _P]),
     "sigb_backward_workspace_size": (_C, [_P, _C, _I, _I, _I, ctypes.POINTER(ctypes.c_size_t)]),
@@ -85,7 +86,7 @@ def check(rc: int) -> None:
 
 
 def set_kernel_policy(policy: int) -> None:
-    """0 = auto (register-resident truncated kernels where available), 1 = generic trie kernels only."""
+    """0 = auto (truncated > fragment > level kernels), 1 = level kernels only, 2 = fragment kernels first."""
     check(lib().sigb_set_kernel_policy(int(policy)))
 
 
@@ -104,3 +105,15 @@ def timing_read(which: int) -> tuple[float, int]:
     n = ctypes.c_int64()
     check(lib().sigb_timing_read(int(which), ctypes.byref(ms), ctypes.byref(n)))
     return float(ms.value), int(n.value)
+
+
+def fragment_plan_info(codes, lengths, d: int) -> dict:
+    """Host-only fragment decomposition of a word set (sigb_fragment_plan_info; no device needed)."""
+    import numpy as np
+
+    c = np.ascontiguousarray(codes, dtype=np.uint64)
+    n = np.ascontiguousarray(lengths, dtype=np.int64)
+    info = np.zeros(8, dtype=np.int64)
+    check(lib().sigb_fragment_plan_info(c.ctypes.data, n.ctypes.data, int(n.size), int(d), info.ctypes.data))
+    keys = ("NC", "G", "K", "fragments", "ctas_per_path", "closure", "cost", "instantiated")
+    return dict(zip(keys, (int(v) for v in info)))

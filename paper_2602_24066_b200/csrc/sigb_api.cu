@@ -160,6 +160,8 @@ int backward_t(const sigb_plan* p, const void* X, int64_t B, int64_t L, const vo
 }
 
 bool use_trunc(const sigb_plan* p) { return g_policy == 0 && p->trunc_depth >= 2 && trunc::supported(p->d, p->trunc_depth); }
+// policy 0: truncated > fragment > level; 1: level only; 2: fragment > level
+bool use_frag(const sigb_plan* p) { return g_policy != 1 && p->frag.ok && !use_trunc(p); }
 
 int check_common(const sigb_plan* p, int dtype, int64_t B, int64_t L) {
   if (!p) return fail(SIGB_ERR_DOMAIN, "plan is NULL");
@@ -175,9 +177,12 @@ int check_common(const sigb_plan* p, int dtype, int64_t B, int64_t L) {
 using namespace sigb;
 
 extern "C" int sigb_version(void) { return 100; }
-extern "C" int sigb_plan_kernel_kind(const sigb_plan* plan) { return plan ? (use_trunc(plan) ? 1 : 0) : -1; }
+extern "C" int sigb_plan_kernel_kind(const sigb_plan* plan) {
+  return plan ? (use_trunc(plan) ? 1 : use_frag(plan) ? 2 : 0) : -1;
+}
 extern "C" int sigb_set_kernel_policy(int policy) {
-  if (policy < 0 || policy > 1) return fail(SIGB_ERR_DOMAIN, "kernel policy must be 0 (auto) or 1 (generic)");
+  if (policy < 0 || policy > 2)
+    return fail(SIGB_ERR_DOMAIN, "kernel policy must be 0 (auto), 1 (level kernels) or 2 (fragment kernels)");
   g_policy = policy;
   return SIGB_OK;
 }
@@ -229,6 +234,8 @@ extern "C" int sigb_forward(const sigb_plan* plan, int dtype, const void* d_X, i
     return trunc::forward(dtype, plan->d, plan->trunc_depth, d_X, B, L, d_out, out_ld, out_col0, include_empty,
                           (cudaStream_t)stream);
   }
+  if (use_frag(plan))
+    return frag::forward(plan, dtype, d_X, B, L, d_out, out_ld, out_col0, include_empty, d_state, (cudaStream_t)stream);
   if (dtype == SIGB_F32)
     return forward_t<float>(plan, d_X, B, L, nullptr, 1, d_out, out_ld, out_col0, include_empty, d_state, nullptr, 0,
                             0, (cudaStream_t)stream);
@@ -258,6 +265,10 @@ extern "C" int sigb_backward_workspace_size(const sigb_plan* plan, int dtype, in
     *bytes = trunc::backward_workspace(dtype, plan->d, plan->trunc_depth, B, L);
     return SIGB_OK;
   }
+  if (use_frag(plan) && ckpt_stride == 0) {
+    *bytes = frag::backward_workspace(plan, dtype, B, L);
+    return SIGB_OK;
+  }
   if (dtype == SIGB_F32) {
     BwdGeometry g = bwd_geometry<float>(plan, B, L, ckpt_stride);
     *bytes = g.partial_bytes + g.ckpt_bytes;
@@ -281,6 +292,11 @@ extern "C" int sigb_backward(const sigb_plan* plan, int dtype, const void* d_X, 
     if (s_is_state) { s_ld = plan->Wc; s_col0 = 0; }
     return trunc::backward(dtype, plan->d, plan->trunc_depth, d_X, B, L, d_S, s_ld, s_col0, d_g, g_ld, g_col0, d_work,
                            work_bytes, d_dX, d_dinc, (cudaStream_t)stream);
+  }
+  if (use_frag(plan) && ckpt_stride == 0 && B > 0 && L > 1) {
+    if (s_is_state) { s_ld = plan->Wc; s_col0 = 0; }
+    return frag::backward(plan, dtype, d_X, B, L, d_S, s_ld, s_col0, d_g, g_ld, g_col0, d_work, work_bytes, d_dX,
+                          d_dinc, (cudaStream_t)stream);
   }
   if (dtype == SIGB_F32)
     return backward_t<float>(plan, d_X, B, L, d_S, s_ld, s_col0, s_is_state, d_g, g_ld, g_col0, ckpt_stride, d_work,

@@ -1,0 +1,155 @@
+// Instantiations and dispatch of the fragment kernels (sigb_frag.cuh).
+#include <algorithm>
+
+#include "sigb_frag.cuh"
+
+namespace sigb {
+namespace frag {
+namespace {
+
+constexpr size_t kPartialBudget = size_t(4) << 30;  // bytes of gradient partials per backward chunk
+
+FragDev dev_of(const sigb_plan* p) {
+  FragDev f;
+  f.letter = p->frag.letter;
+  f.cidx = p->frag.cidx;
+  f.eidx = p->frag.eidx;
+  f.sidx = p->frag.sidx;
+  f.red_idx = p->frag.red_idx;
+  f.red_off = p->frag.red_off;
+  f.Fp = p->frag.Fp;
+  f.cpp = p->frag.cpp;
+  f.d = (int)p->d;
+  return f;
+}
+
+template <typename T, int NC, int G, int K>
+int fwd(const sigb_plan* p, const T* X, int64_t B, int64_t L, T* out, int64_t out_ld, int64_t out_col0,
+        int include_empty, T* state, cudaStream_t stream) {
+  const int d = (int)p->d;
+  const int64_t grid = B * p->frag.cpp;
+  if (grid == 0) return SIGB_OK;
+  const size_t smem = sizeof(T) * ((size_t)(kChunkF + 1) * d + (size_t)kChunkF * (d + 1));
+  if (smem > 48 * 1024)
+    SIGB_CUDA_TRY(cudaFuncSetAttribute(frag_forward_kernel<T, NC, G, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+  count_launch();
+  timing_begin(0, stream);
+  frag_forward_kernel<T, NC, G, K><<<(unsigned)grid, kTPB, smem, stream>>>(dev_of(p), X, L, out, out_ld, out_col0,
+                                                                            include_empty, state, p->Wc);
+  timing_end(0, stream);
+  SIGB_CUDA_TRY(cudaGetLastError());
+  return SIGB_OK;
+}
+
+template <typename T>
+int64_t bwd_chunk(const sigb_plan* p, int64_t B, int64_t L) {
+  const size_t per_path = sizeof(T) * (size_t)p->frag.cpp * (size_t)(L - 1) * p->d;
+  int64_t c = per_path ? (int64_t)(kPartialBudget / per_path) : B;
+  return std::max<int64_t>(1, std::min(c, B));
+}
+
+template <typename T>
+__global__ void frag_sample_grads(const T* __restrict__ partial, int64_t Bc, int64_t P, int64_t M, int64_t d,
+                                  int64_t b0, T* __restrict__ dX, T* __restrict__ dinc) {
+  const int64_t L = M + 1;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= Bc * L * d) return;
+  const int64_t z = i % d, t = (i / d) % L, bl = i / (d * L);
+  auto inc = [&](int64_t j) {
+    T s = T(0);
+    for (int64_t q = 0; q < P; ++q) s += partial[((bl * P + q) * M + j) * d + z];
+    return s;
+  };
+  T v = T(0);
+  if (t >= 1) v += inc(t - 1);
+  if (t < M) {
+    const T it = inc(t);
+    v -= it;
+    if (dinc) dinc[((b0 + bl) * M + t) * d + z] = it;
+  }
+  dX[((b0 + bl) * L + t) * d + z] = v;
+}
+
+template <typename T, int NC, int G, int K>
+int bwd(const sigb_plan* p, const T* X, int64_t B, int64_t L, const T* S, int64_t s_ld, int64_t s_col0, const T* g,
+        int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, T* dX, T* dinc, cudaStream_t stream) {
+  const int d = (int)p->d;
+  const int64_t M = L - 1;
+  const int cpp = p->frag.cpp;
+  const int64_t chunk = bwd_chunk<T>(p, B, L);
+  const size_t need = sizeof(T) * (size_t)chunk * cpp * M * d;
+  if (!work || work_bytes < need) return fail(SIGB_ERR_DOMAIN, "backward workspace too small");
+  const size_t smem = sizeof(T) * bwd_smem_elems<NC, G, K>(d) + sizeof(unsigned short) * (size_t)p->frag.max_red + 16;
+  SIGB_CUDA_TRY(cudaFuncSetAttribute(frag_backward_kernel<T, NC, G, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+  T* partial = (T*)work;
+  for (int64_t b0 = 0; b0 < B; b0 += chunk) {
+    const int64_t Bc = std::min(chunk, B - b0);
+    count_launch(2);
+    timing_begin(1, stream);
+    frag_backward_kernel<T, NC, G, K><<<(unsigned)(Bc * cpp), kTPB, smem, stream>>>(dev_of(p), X, L, b0, S, s_ld,
+                                                                                    s_col0, g, g_ld, g_col0, partial);
+    timing_end(1, stream);
+    SIGB_CUDA_TRY(cudaGetLastError());
+    const int64_t n = Bc * L * d;
+    frag_sample_grads<T><<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(partial, Bc, cpp, M, d, b0, dX, dinc);
+    SIGB_CUDA_TRY(cudaGetLastError());
+  }
+  return SIGB_OK;
+}
+
+#define SIGB_FRAG_GK(X, NC) X(NC, 5, 5) X(NC, 4, 4) X(NC, 2, 8) X(NC, 1, 16)
+#define SIGB_FRAG_CASES(X) SIGB_FRAG_GK(X, 1) SIGB_FRAG_GK(X, 2) SIGB_FRAG_GK(X, 3) SIGB_FRAG_GK(X, 4) SIGB_FRAG_GK(X, 5)
+
+}  // namespace
+
+bool supported(int NC, int G, int K) {
+#define X(a, b, c) \
+  if (NC == a && G == b && K == c) return true;
+  SIGB_FRAG_CASES(X)
+#undef X
+  return false;
+}
+
+int forward(const sigb_plan* p, int dtype, const void* Xv, int64_t B, int64_t L, void* out, int64_t out_ld,
+            int64_t out_col0, int include_empty, void* state, cudaStream_t stream) {
+  const int NC = p->frag.NC, G = p->frag.G, K = p->frag.K;
+#define X(a, b, c)                                                                                               \
+  if (NC == a && G == b && K == c) {                                                                             \
+    if (dtype == SIGB_F32)                                                                                       \
+      return fwd<float, a, b, c>(p, (const float*)Xv, B, L, (float*)out, out_ld, out_col0, include_empty,        \
+                                 (float*)state, stream);                                                         \
+    return fwd<double, a, b, c>(p, (const double*)Xv, B, L, (double*)out, out_ld, out_col0, include_empty,       \
+                                (double*)state, stream);                                                         \
+  }
+  SIGB_FRAG_CASES(X)
+#undef X
+  return fail(SIGB_ERR_UNSUPPORTED, "no fragment kernel for this shape");
+}
+
+size_t backward_workspace(const sigb_plan* p, int dtype, int64_t B, int64_t L) {
+  const size_t es = dtype == SIGB_F32 ? 4 : 8;
+  const int64_t chunk = dtype == SIGB_F32 ? bwd_chunk<float>(p, B, L) : bwd_chunk<double>(p, B, L);
+  return es * (size_t)chunk * p->frag.cpp * (size_t)(L - 1) * p->d;
+}
+
+int backward(const sigb_plan* p, int dtype, const void* Xv, int64_t B, int64_t L, const void* S, int64_t s_ld,
+             int64_t s_col0, const void* g, int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, void* dX,
+             void* dinc, cudaStream_t stream) {
+  const int NC = p->frag.NC, G = p->frag.G, K = p->frag.K;
+#define X(a, b, c)                                                                                                 \
+  if (NC == a && G == b && K == c) {                                                                               \
+    if (dtype == SIGB_F32)                                                                                         \
+      return bwd<float, a, b, c>(p, (const float*)Xv, B, L, (const float*)S, s_ld, s_col0, (const float*)g, g_ld,  \
+                                 g_col0, work, work_bytes, (float*)dX, (float*)dinc, stream);                      \
+    return bwd<double, a, b, c>(p, (const double*)Xv, B, L, (const double*)S, s_ld, s_col0, (const double*)g,      \
+                                g_ld, g_col0, work, work_bytes, (double*)dX, (double*)dinc, stream);               \
+  }
+  SIGB_FRAG_CASES(X)
+#undef X
+  return fail(SIGB_ERR_UNSUPPORTED, "no fragment kernel for this shape");
+}
+
+}  // namespace frag
+}  // namespace sigb

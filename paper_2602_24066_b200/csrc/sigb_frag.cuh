@@ -1,0 +1,385 @@
+// Register-resident Chen kernels for ARBITRARY prefix-closed tries
+// (anisotropic truncations, user word sets: configs 3 and 4 of BASELINE.json,
+// and full truncations without a dedicated sigb_trunc instantiation).
+//
+// Work decomposition (built by the planner in sigb_plan.cu).  Every thread
+// owns one FRAGMENT of the trie for the whole time sweep, in registers:
+//   - an anchor node a (any internal node whose children are not all leaves,
+//     or the empty word) and its chain of ancestors,
+//   - up to G "mids": children of a whose own children are all leaves,
+//   - for every mid, up to K leaf children drawn from one fragment-wide list
+//     of K letters LL (a mid that lacks LL[k] simply carries a dead register),
+//   - up to K leaf children of a itself ("anchor leaves", letters AL).
+// The generalisation of sigb_trunc's fragment is the chain: its length (the
+// anchor's level) varies per thread, so chains are RIGHT-ALIGNED to a common
+// length NC and padded at the front with identity nodes (S = 1, increment 0),
+// for which the Horner recursion reproduces T(eps, m) = 1 exactly.  All levels
+// are then "virtual" (real level + NC - |a|); the Horner factors 1/(m-|u|+1)
+// only see level differences, so they are unchanged.
+//
+// Forward step per thread (PAPER.md:190-216 in the shared-prefix form of
+// sigb_level.cu):  sum_{k<NC} (NV-k) chain + 2G mid + G*K leaf + K anchor-leaf
+// FMAs, NV = NC + 2.  Increments are gathered per step from a shared-memory row
+// (one LDS per letter slot; the row carries a zero column at index d for empty
+// slots).
+//
+// Backward: the memory-lean reverse sweep of sigb_trunc (rebuild S by
+// exp(-dX), partials, reverse mode; leaf adjoints are constant in time).  The
+// per-step gradient terms of a thread belong to letters known only at run
+// time, so they are parked in shared memory (slot-major, conflict-free) and
+// summed per letter through the plan's fixed-order CSR lists: deterministic,
+// no atomics.
+#pragma once
+
+#include "sigb_internal.h"
+
+namespace sigb {
+namespace frag {
+
+constexpr int kTPB = 128;      // threads (fragments) per CTA
+constexpr int kChunkF = 16;    // steps of samples staged per chunk
+constexpr int kRedSteps = 4;   // steps per gradient-reduction round (bwd)
+
+template <int NC, int G, int K>
+struct Shape {
+  static constexpr int NV = NC + 2;                 // virtual depth
+  static constexpr int NS = NC + G + G * K + K;     // state slots
+  static constexpr int NGS = NC + G + 2 * K;        // letter / gradient slots
+  // slot order (state): chain [0,NC) | mids [NC,NC+G) | leaves [.., +G*K) g-major | anchor leaves
+  // slot order (letters): chain | mids | LL[K] | AL[K]
+};
+
+template <typename T, int NC, int G, int K>
+struct FState {
+  T ch[NC];
+  T mid[G];
+  T leaf[G][K];
+  T al[K];
+};
+
+template <typename T, int NC, int G, int K>
+struct FIncr {
+  T dc[NC];
+  T dy[G];
+  T dz[K];
+  T da[K];
+};
+
+template <typename T>
+__device__ __forceinline__ T rinv(int r) {
+  return T(1) / T(r);
+}
+
+// Per-thread letter offsets into the staged increment row (letter d = zero column).
+template <int NC, int G, int K>
+struct Letters {
+  int c[NC], y[G], z[K], a[K];
+};
+
+template <typename T, int NC, int G, int K>
+__device__ __forceinline__ void gather(const T* __restrict__ row, const Letters<NC, G, K>& lt, T sign,
+                                       FIncr<T, NC, G, K>& in) {
+#pragma unroll
+  for (int k = 0; k < NC; ++k) in.dc[k] = sign * row[lt.c[k]];
+#pragma unroll
+  for (int g = 0; g < G; ++g) in.dy[g] = sign * row[lt.y[g]];
+#pragma unroll
+  for (int k = 0; k < K; ++k) in.dz[k] = sign * row[lt.z[k]];
+#pragma unroll
+  for (int k = 0; k < K; ++k) in.da[k] = sign * row[lt.a[k]];
+}
+
+// tch[k][m] = T(chain_k, m), m = k+1 .. NV (virtual levels).
+template <typename T, int NC, int G, int K>
+__device__ __forceinline__ void chain_partials(const FState<T, NC, G, K>& st, const FIncr<T, NC, G, K>& in,
+                                               T (&tch)[NC][NC + 3]) {
+  constexpr int NV = NC + 2;
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    const int lv = k + 1;
+#pragma unroll
+    for (int m = lv; m <= NV; ++m) {
+      const T a = (m == lv) ? in.dc[k] : in.dc[k] * rinv<T>(m - lv + 1);
+      tch[k][m] = (k == 0) ? st.ch[k] + a : fma(a, tch[k > 0 ? k - 1 : 0][m], st.ch[k]);
+    }
+  }
+}
+
+template <typename T, int NC, int G, int K>
+__device__ __forceinline__ void chen_step(FState<T, NC, G, K>& st, const FIncr<T, NC, G, K>& in) {
+  constexpr int NV = NC + 2;
+  T tch[NC][NC + 3];
+  chain_partials<T, NC, G, K>(st, in, tch);
+  const T tN1 = tch[NC - 1][NV - 1];
+  const T tN = tch[NC - 1][NV];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) st.ch[k] = tch[k][k + 1];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const T tm = fma(in.dy[g] * T(0.5), tN, st.mid[g]);  // T(mid_g, NV)
+    st.mid[g] = fma(in.dy[g], tN1, st.mid[g]);
+#pragma unroll
+    for (int k = 0; k < K; ++k) st.leaf[g][k] = fma(in.dz[k], tm, st.leaf[g][k]);
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) st.al[k] = fma(in.da[k], tN1, st.al[k]);
+}
+
+// Device view of a fragment plan.  Per-fragment arrays are slot-major
+// ([slot][Fp]) so that a warp's loads are coalesced.
+struct FragDev {
+  const unsigned char* letter;  // [NGS][Fp] letter of the slot, d = none
+  const int* cidx;              // [NS][Fp] closure index to read S (-1 empty, -2 identity)
+  const int* eidx;              // [NS][Fp] emitted index in I (owner only) or -1
+  const int* sidx;              // [NS][Fp] closure index to write state (owner only) or -1
+  const unsigned short* red_idx;  // per CTA-part CSR entries (slot * kTPB + tid), fixed order
+  const int* red_off;           // [cpp][d + 1] (offsets into red_idx, absolute)
+  int Fp, cpp, d;
+};
+
+template <int NC, int G, int K>
+__device__ __forceinline__ void load_letters(const FragDev& fd, int f, Letters<NC, G, K>& lt) {
+  using SH = Shape<NC, G, K>;
+  const unsigned char* L = fd.letter + f;
+#pragma unroll
+  for (int k = 0; k < NC; ++k) lt.c[k] = L[(size_t)k * fd.Fp];
+#pragma unroll
+  for (int g = 0; g < G; ++g) lt.y[g] = L[(size_t)(NC + g) * fd.Fp];
+#pragma unroll
+  for (int k = 0; k < K; ++k) lt.z[k] = L[(size_t)(NC + G + k) * fd.Fp];
+#pragma unroll
+  for (int k = 0; k < K; ++k) lt.a[k] = L[(size_t)(NC + G + K + k) * fd.Fp];
+  (void)SH::NS;
+}
+
+// Visit every state slot with its flat index (slot order of Shape).
+template <typename T, int NC, int G, int K, typename F>
+__device__ __forceinline__ void for_slots(FState<T, NC, G, K>& st, F&& fn) {
+#pragma unroll
+  for (int k = 0; k < NC; ++k) fn(k, st.ch[k]);
+#pragma unroll
+  for (int g = 0; g < G; ++g) fn(NC + g, st.mid[g]);
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int k = 0; k < K; ++k) fn(NC + G + g * K + k, st.leaf[g][k]);
+#pragma unroll
+  for (int k = 0; k < K; ++k) fn(NC + G + G * K + k, st.al[k]);
+}
+
+// Stage samples [j0, j0+cs] of path b and write increments Dl[s][z] (row
+// stride d+1, zero at column d).
+template <typename T>
+__device__ __forceinline__ void stage(const T* __restrict__ Xb, int d, int j0, int cs, T* __restrict__ Xs,
+                                      T* __restrict__ Dl) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const T* src = Xb + (int64_t)j0 * d;
+  for (int i = tid; i < (cs + 1) * d; i += nt) Xs[i] = src[i];
+  __syncthreads();
+  const int rs = d + 1;
+  for (int i = tid; i < cs * rs; i += nt) {
+    const int s = i / rs, z = i % rs;
+    Dl[i] = z < d ? Xs[(s + 1) * d + z] - Xs[s * d + z] : T(0);
+  }
+  __syncthreads();
+}
+
+template <typename T, int NC, int G, int K>
+__global__ void __launch_bounds__(kTPB) frag_forward_kernel(FragDev fd, const T* __restrict__ X, int64_t L,
+                                                            T* __restrict__ out, int64_t out_ld, int64_t out_col0,
+                                                            int include_empty, T* __restrict__ state, int64_t Wc) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Xs = reinterpret_cast<T*>(smem_raw);
+  T* Dl = Xs + (kChunkF + 1) * fd.d;
+  const int64_t b = blockIdx.x / fd.cpp;
+  const int f = (int)(blockIdx.x % fd.cpp) * kTPB + threadIdx.x;
+  Letters<NC, G, K> lt;
+  load_letters<NC, G, K>(fd, f, lt);
+  FState<T, NC, G, K> st;
+  for_slots<T, NC, G, K>(st, [&](int i, T& v) { v = fd.cidx[(size_t)i * fd.Fp + f] == -2 ? T(1) : T(0); });
+  const int64_t M = L - 1;
+  const T* Xb = X + b * L * fd.d;
+  for (int64_t j0 = 0; j0 < M; j0 += kChunkF) {
+    const int cs = (int)(M - j0 < kChunkF ? M - j0 : kChunkF);
+    stage<T>(Xb, fd.d, (int)j0, cs, Xs, Dl);
+#pragma unroll 1
+    for (int s = 0; s < cs; ++s) {
+      FIncr<T, NC, G, K> in;
+      gather<T, NC, G, K>(Dl + s * (fd.d + 1), lt, T(1), in);
+      chen_step<T, NC, G, K>(st, in);
+    }
+    __syncthreads();
+  }
+  T* orow = out ? out + b * out_ld + out_col0 : nullptr;
+  T* srow = state ? state + b * Wc : nullptr;
+  for_slots<T, NC, G, K>(st, [&](int i, T& v) {
+    const int e = fd.eidx[(size_t)i * fd.Fp + f];
+    if (orow && e >= 0) orow[e] = v;
+    if (srow) {
+      const int si = fd.sidx[(size_t)i * fd.Fp + f];
+      if (si >= 0) srow[si] = v;
+    }
+  });
+  if (orow && include_empty && f == 0) orow[-1] = T(1);
+}
+
+template <int NC, int G, int K>
+__host__ __device__ constexpr size_t bwd_smem_elems(int d) {
+  return (size_t)(kChunkF + 1) * d + (size_t)kChunkF * (d + 1) +
+         (size_t)kRedSteps * Shape<NC, G, K>::NGS * kTPB;
+}
+
+// Backward over paths [b0, b0 + gridDim.x / cpp).  partial layout:
+// [(b - b0) * cpp + cip][M][d] (fixed-order sums of this CTA's fragments).
+template <typename T, int NC, int G, int K>
+__global__ void __launch_bounds__(kTPB) frag_backward_kernel(FragDev fd, const T* __restrict__ X, int64_t L,
+                                                             int64_t b0, const T* __restrict__ Sin, int64_t s_ld,
+                                                             int64_t s_col0, const T* __restrict__ gup,
+                                                             int64_t g_ld, int64_t g_col0, T* __restrict__ partial) {
+  using SH = Shape<NC, G, K>;
+  constexpr int NV = SH::NV;
+  constexpr int NGS = SH::NGS;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int d = fd.d;
+  T* Xs = reinterpret_cast<T*>(smem_raw);
+  T* Dl = Xs + (kChunkF + 1) * d;
+  T* buf = Dl + kChunkF * (d + 1);  // [kRedSteps][NGS][kTPB]
+  const int cip = (int)(blockIdx.x % fd.cpp);
+  const int64_t bl = blockIdx.x / fd.cpp, b = b0 + bl;
+  const int tid = threadIdx.x;
+  const int f = cip * kTPB + tid;
+  const int64_t M = L - 1;
+  Letters<NC, G, K> lt;
+  load_letters<NC, G, K>(fd, f, lt);
+  FState<T, NC, G, K> st, lam;
+  {
+    const T* srow = Sin + b * s_ld + s_col0;
+    const T* grow = gup + b * g_ld + g_col0;
+    for_slots<T, NC, G, K>(st, [&](int i, T& v) {
+      const int c = fd.cidx[(size_t)i * fd.Fp + f];
+      v = c == -2 ? T(1) : (c >= 0 ? srow[c] : T(0));
+    });
+    for_slots<T, NC, G, K>(lam, [&](int i, T& v) {
+      const int e = fd.eidx[(size_t)i * fd.Fp + f];
+      v = e >= 0 ? grow[e] : T(0);
+    });
+  }
+  // reduction geometry: rsplit lanes per letter (power of two <= 32)
+  int rsplit = 1;
+  while (rsplit * 2 <= 32 && rsplit * 2 * d <= kTPB) rsplit *= 2;
+  const int* roff = fd.red_off + cip * (d + 1);
+  // this CTA-part's reduction list, staged once (u16 offsets into buf)
+  unsigned short* rl = reinterpret_cast<unsigned short*>(buf + (size_t)kRedSteps * NGS * kTPB);
+  const int rbase = roff[0];
+  for (int i = tid; i < roff[d] - rbase; i += kTPB) rl[i] = fd.red_idx[rbase + i];
+  const T* Xb = X + b * L * d;
+  T* pout = partial + (bl * fd.cpp + cip) * M * d;
+  const int nchunks = (int)((M + kChunkF - 1) / kChunkF);
+  for (int c = nchunks - 1; c >= 0; --c) {
+    const int j0 = c * kChunkF;
+    const int cs = (int)(M - j0 < kChunkF ? M - j0 : kChunkF);
+    stage<T>(Xb, d, j0, cs, Xs, Dl);
+    int nbuf = 0;  // steps parked in buf
+#pragma unroll 1
+    for (int s = cs - 1; s >= 0; --s) {
+      const T* row = Dl + s * (d + 1);
+      FIncr<T, NC, G, K> in;
+      // (a) S_{0,t_{j+1}} -> S_{0,t_j}
+      gather<T, NC, G, K>(row, lt, T(-1), in);
+      chen_step<T, NC, G, K>(st, in);
+      // (b) forward partials from S_{0,t_j}
+      gather<T, NC, G, K>(row, lt, T(1), in);
+      T tch[NC][NC + 3];
+      chain_partials<T, NC, G, K>(st, in, tch);
+      const T tN1 = tch[NC - 1][NV - 1];
+      const T tN = tch[NC - 1][NV];
+      // (c) reverse: leaves, mids, anchor leaves, chain
+      T gl[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) gl[k] = T(0);
+      T gm[G];
+      T tbp1 = T(0), tbp2 = T(0);  // Tbar(anchor, NV-1), Tbar(anchor, NV)
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const T tm = fma(in.dy[g] * T(0.5), tN, st.mid[g]);
+        T tb = T(0);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          tb = fma(in.dz[k], lam.leaf[g][k], tb);
+          gl[k] = fma(lam.leaf[g][k], tm, gl[k]);
+        }
+        const T lm = lam.mid[g];
+        tbp1 = fma(in.dy[g], lm, tbp1);
+        tbp2 = fma(in.dy[g] * T(0.5), tb, tbp2);
+        gm[g] = fma(lm, tN1, tb * tN * T(0.5));
+        lam.mid[g] = lm + tb;
+      }
+      T ga[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        tbp1 = fma(in.da[k], lam.al[k], tbp1);
+        ga[k] = lam.al[k] * tN1;
+      }
+      T gch[NC];
+      {
+        T tbc[NV + 1];
+#pragma unroll
+        for (int m = 0; m <= NV; ++m) tbc[m] = T(0);
+        tbc[NV - 1] = tbp1;
+        tbc[NV] = tbp2;
+#pragma unroll
+        for (int k = NC - 1; k >= 0; --k) {
+          const int lv = k + 1;
+          T tbn[NV + 1];
+#pragma unroll
+          for (int m = 0; m <= NV; ++m) tbn[m] = (m == lv) ? lam.ch[k] : tbc[m];
+          T lsum = tbn[lv];
+          T gs = T(0);
+#pragma unroll
+          for (int m = lv; m <= NV; ++m) {
+            if (m > lv) lsum += tbn[m];
+            const T par = (k == 0) ? T(1) : tch[k > 0 ? k - 1 : 0][m];
+            gs = (m == lv) ? fma(tbn[m], par, gs) : fma(tbn[m] * rinv<T>(m - lv + 1), par, gs);
+          }
+          lam.ch[k] = lsum;
+          gch[k] = gs;
+#pragma unroll
+          for (int m = 0; m <= NV; ++m)
+            tbc[m] = (m >= lv) ? ((m == lv) ? in.dc[k] : in.dc[k] * rinv<T>(m - lv + 1)) * tbn[m] : T(0);
+        }
+      }
+      // (d) park this step's gradient terms (slot-major, conflict-free)
+      T* pb = buf + (size_t)nbuf * NGS * kTPB + tid;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) pb[k * kTPB] = gch[k];
+#pragma unroll
+      for (int g = 0; g < G; ++g) pb[(NC + g) * kTPB] = gm[g];
+#pragma unroll
+      for (int k = 0; k < K; ++k) pb[(NC + G + k) * kTPB] = gl[k];
+#pragma unroll
+      for (int k = 0; k < K; ++k) pb[(NC + G + K + k) * kTPB] = ga[k];
+      ++nbuf;
+      if (nbuf == kRedSteps || s == 0) {
+        __syncthreads();
+        // per (parked step, letter): fixed-order CSR sum, rsplit lanes per letter
+        for (int r = 0; r < nbuf; ++r) {
+          const T* pr = buf + (size_t)r * NGS * kTPB;
+          const int jstep = j0 + s + (nbuf - 1 - r);  // buf[0] holds the latest (largest) step
+          for (int z0 = 0; z0 < d; z0 += kTPB / rsplit) {
+            const int z = z0 + tid / rsplit, sub = tid % rsplit;
+            T acc = T(0);
+            if (z < d)
+              for (int e = roff[z] - rbase + sub; e < roff[z + 1] - rbase; e += rsplit) acc += pr[rl[e]];
+            for (int o = rsplit / 2; o > 0; o /= 2) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (z < d && sub == 0) pout[(int64_t)jstep * d + z] = acc;
+          }
+        }
+        __syncthreads();
+        nbuf = 0;
+      }
+    }
+  }
+}
+
+}  // namespace frag
+}  // namespace sigb

@@ -55,6 +55,45 @@ struct PlanDev {
   int max_len;
 };
 
+// Prefix closure cl(I) of a word set as a trie, canonical (length, code) order.
+struct Trie {
+  int64_t d = 0;
+  int max_len = 0;
+  std::vector<uint64_t> code;   // closure, canonical order
+  std::vector<int64_t> len;
+  std::vector<int64_t> parent;  // closure index, -1 for the empty word
+  std::vector<int64_t> child_first, child_count;
+  std::vector<int> md;          // deepest descendant length (incl. self)
+  std::vector<int64_t> cost;    // subtree shared-memory cost (elements)
+  std::vector<int64_t> emit;    // emitted index in I or -1
+};
+
+// Host image of a fragment plan (sigb_frag.cuh).  Per-fragment arrays are
+// slot-major: [slot][Fp].
+struct FragHost {
+  int NC = 0, G = 0, K = 0;  // template shape
+  int F = 0, cpp = 0, Fp = 0;
+  double cost = 0;           // estimated issue slots per path-step (forward)
+  std::vector<unsigned char> letter;  // [NGS][Fp], d = none
+  std::vector<int> cidx, eidx, sidx;  // [NS][Fp]
+  std::vector<unsigned short> red_idx;
+  std::vector<int> red_off;  // [cpp][d+1] absolute offsets into red_idx
+  int max_red = 0;           // largest per-CTA list (entries)
+};
+
+// Builds the fragment decomposition of `t` for the best available template
+// shape; false (with `why`) when no instantiation fits.
+bool plan_fragments(const Trie& t, FragHost& out, std::string& why);
+
+struct FragDevPlan {
+  bool ok = false;
+  int NC = 0, G = 0, K = 0, F = 0, cpp = 0, Fp = 0, max_red = 0;
+  unsigned char* letter = nullptr;
+  int *cidx = nullptr, *eidx = nullptr, *sidx = nullptr;
+  unsigned short* red_idx = nullptr;
+  int* red_off = nullptr;
+};
+
 }  // namespace sigb
 
 struct sigb_plan {
@@ -75,6 +114,7 @@ struct sigb_plan {
   int* d_perm = nullptr;
   int* d_lseg = nullptr;
   std::vector<sigb::PartDesc> h_parts;
+  sigb::FragDevPlan frag;  // register-resident fragment kernels (sigb_frag.cuh), when ok
 
   sigb::PlanDev dev() const {
     sigb::PlanDev p;
@@ -98,6 +138,15 @@ void count_launch(int n = 1);
 // `which` 0 = forward Chen kernel, 1 = backward Chen kernel (summed over batch chunks).
 void timing_begin(int which, cudaStream_t stream);
 void timing_end(int which, cudaStream_t stream);
+namespace frag {
+bool supported(int NC, int G, int K);
+int forward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, void* out, int64_t out_ld,
+            int64_t out_col0, int include_empty, void* state, cudaStream_t stream);
+size_t backward_workspace(const sigb_plan* p, int dtype, int64_t B, int64_t L);
+int backward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, const void* S, int64_t s_ld,
+             int64_t s_col0, const void* g, int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, void* dX,
+             void* dinc, cudaStream_t stream);
+}  // namespace frag
 namespace trunc {
 bool supported(int64_t d, int depth);
 int forward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L, void* out, int64_t out_ld,

@@ -22,18 +22,6 @@ namespace {
 // Shared-memory budget a part's backward may use, in bytes, at 8-byte elements.
 constexpr int64_t kPartSmemBudget = 200 * 1024;
 
-struct Trie {
-  int64_t d = 0;
-  int max_len = 0;
-  std::vector<uint64_t> code;   // closure, canonical order
-  std::vector<int64_t> len;
-  std::vector<int64_t> parent;  // closure index, -1 for the empty word
-  std::vector<int64_t> child_first, child_count;
-  std::vector<int> md;          // deepest descendant length (incl. self)
-  std::vector<int64_t> cost;    // subtree shared-memory cost (elements)
-  std::vector<int64_t> emit;    // emitted index in I or -1
-};
-
 int64_t node_cost(int level, int md) { return 3 + (md - level) + (md - level + 1); }
 
 struct PartSpec {
@@ -68,11 +56,12 @@ void split(const Trie& t, const std::vector<int64_t>& chain, int64_t first, int6
 
 using namespace sigb;
 
-extern "C" int sigb_plan_create(const uint64_t* codes, const int64_t* lengths, int64_t W, int64_t d,
-                                sigb_plan** plan_out, void* stream_) {
-  if (!plan_out) return fail(SIGB_ERR_DOMAIN, "plan output pointer is NULL");
-  *plan_out = nullptr;
-  cudaStream_t stream = (cudaStream_t)stream_;
+// Builds the prefix closure cl(I) as a trie.  The parent of w is
+// prefix_table[w, |w|-1]: taken from the DEVICE table builder
+// (sigb_wordset_tables) when `stream_or_null` is a live stream, else by the
+// same binary search on the host (sigb_fragment_plan_info, no GPU needed).
+static int build_trie(const uint64_t* codes, const int64_t* lengths, int64_t W, int64_t d, bool on_device,
+                      cudaStream_t stream, Trie& t) {
   if (W < 1) return fail(SIGB_ERR_DOMAIN, "word set has no words to compute");
   if (d < 1) return fail(SIGB_ERR_DOMAIN, "alphabet size must be >= 1, got " + std::to_string(d));
   if (d > 255) return fail(SIGB_ERR_UNSUPPORTED, "the device kernels support d <= 255 letters");
@@ -96,7 +85,7 @@ extern "C" int sigb_plan_create(const uint64_t* codes, const int64_t* lengths, i
       cl.emplace_back(k, k == lengths[i] ? codes[i] : codes[i] / pw[lengths[i] - k]);
   std::sort(cl.begin(), cl.end());
   cl.erase(std::unique(cl.begin(), cl.end()), cl.end());
-  Trie t;
+  t = Trie();
   t.d = d;
   t.max_len = (int)max_len;
   const int64_t Wc = (int64_t)cl.size();
@@ -111,9 +100,9 @@ extern "C" int sigb_plan_create(const uint64_t* codes, const int64_t* lengths, i
       t.emit[j] = i;
     }
   }
-  // -- device tables of the closure; the parent of w is prefix_table[w, |w|-1] --
-  std::vector<int64_t> prefix((size_t)Wc * (max_len + 1));
-  {
+  t.parent.resize(Wc);
+  if (on_device) {
+    std::vector<int64_t> prefix((size_t)Wc * (max_len + 1));
     uint64_t* dc = nullptr;
     int64_t *dl = nullptr, *dp = nullptr, *ds = nullptr;
     SIGB_CUDA_TRY(cudaMalloc(&dc, sizeof(uint64_t) * Wc));
@@ -128,14 +117,19 @@ extern "C" int sigb_plan_create(const uint64_t* codes, const int64_t* lengths, i
                                   stream));
     SIGB_CUDA_TRY(cudaStreamSynchronize(stream));
     cudaFree(dc); cudaFree(dl); cudaFree(dp); cudaFree(ds);
+    for (int64_t i = 0; i < Wc; ++i) t.parent[i] = t.len[i] == 1 ? -1 : prefix[(size_t)i * (max_len + 1) + t.len[i] - 1];
+  } else {
+    for (int64_t i = 0; i < Wc; ++i) {
+      if (t.len[i] == 1) { t.parent[i] = -1; continue; }
+      const std::pair<int64_t, uint64_t> key(t.len[i] - 1, t.code[i] / (uint64_t)d);
+      auto it = std::lower_bound(cl.begin(), cl.end(), key);
+      t.parent[i] = (it != cl.end() && *it == key) ? (int64_t)(it - cl.begin()) : -2;
+    }
   }
-  t.parent.resize(Wc);
   t.child_first.assign(Wc, 0);
   t.child_count.assign(Wc, 0);
-  for (int64_t i = 0; i < Wc; ++i) {
-    t.parent[i] = t.len[i] == 1 ? -1 : prefix[(size_t)i * (max_len + 1) + t.len[i] - 1];
+  for (int64_t i = 0; i < Wc; ++i)
     if (t.len[i] > 1 && t.parent[i] < 0) return fail(SIGB_ERR_CUDA, "closure lost a prefix (table build failed)");
-  }
   for (int64_t i = Wc - 1; i >= 0; --i) {
     int64_t p = t.parent[i];
     if (p >= 0) { t.child_first[p] = i; t.child_count[p] += 1; }
@@ -152,6 +146,35 @@ extern "C" int sigb_plan_create(const uint64_t* codes, const int64_t* lengths, i
     for (int64_t k = t.child_first[i]; k < t.child_first[i] + t.child_count[i]; ++k) c += t.cost[k];
     t.cost[i] = c;
   }
+  return SIGB_OK;
+}
+
+extern "C" int sigb_fragment_plan_info(const uint64_t* codes, const int64_t* lengths, int64_t W, int64_t d,
+                                       int64_t* info) {
+  if (!info) return fail(SIGB_ERR_DOMAIN, "info output pointer is NULL");
+  Trie t;
+  int rc = build_trie(codes, lengths, W, d, false, nullptr, t);
+  if (rc) return rc;
+  FragHost fh;
+  std::string why;
+  if (!plan_fragments(t, fh, why)) return fail(SIGB_ERR_UNSUPPORTED, why);
+  info[0] = fh.NC; info[1] = fh.G; info[2] = fh.K; info[3] = fh.F; info[4] = fh.cpp;
+  info[5] = (int64_t)t.code.size(); info[6] = (int64_t)fh.cost; info[7] = frag::supported(fh.NC, fh.G, fh.K);
+  return SIGB_OK;
+}
+
+extern "C" int sigb_plan_create(const uint64_t* codes, const int64_t* lengths, int64_t W, int64_t d,
+                                sigb_plan** plan_out, void* stream_) {
+  if (!plan_out) return fail(SIGB_ERR_DOMAIN, "plan output pointer is NULL");
+  *plan_out = nullptr;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  Trie t;
+  {
+    int rc = build_trie(codes, lengths, W, d, true, stream, t);
+    if (rc) return rc;
+  }
+  const int64_t Wc = (int64_t)t.code.size();
+  const int64_t max_len = t.max_len;
   // -- partition into parts -----------------------------------------------------
   const int64_t fixed = (int64_t)(kChunk + 1) * d + (int64_t)kChunk * max_len * d + 64;
   const int64_t budget = std::max<int64_t>(kPartSmemBudget / 8 - fixed, 64);
@@ -273,6 +296,30 @@ extern "C" int sigb_plan_create(const uint64_t* codes, const int64_t* lengths, i
     plan->h_parts.push_back(pd);
   }
   plan->step_fmas = step_fmas;
+  // register-resident fragment plan (sigb_frag.cuh) for the generic path
+  {
+    FragHost fh;
+    std::string why;
+    if (plan_fragments(t, fh, why) && frag::supported(fh.NC, fh.G, fh.K)) {
+      FragDevPlan& fp = plan->frag;
+      fp.NC = fh.NC; fp.G = fh.G; fp.K = fh.K; fp.F = fh.F; fp.cpp = fh.cpp; fp.Fp = fh.Fp;
+      fp.max_red = fh.max_red;
+      int rc2;
+      auto up = [&](auto** dst, const auto& src) -> int {
+        using E = typename std::remove_reference<decltype(src)>::type::value_type;
+        SIGB_CUDA_TRY(cudaMalloc((void**)dst, sizeof(E) * std::max<size_t>(src.size(), 1)));
+        if (!src.empty())
+          SIGB_CUDA_TRY(cudaMemcpyAsync((void*)*dst, src.data(), sizeof(E) * src.size(), cudaMemcpyHostToDevice, stream));
+        return SIGB_OK;
+      };
+      if ((rc2 = up(&fp.letter, fh.letter)) || (rc2 = up(&fp.cidx, fh.cidx)) || (rc2 = up(&fp.eidx, fh.eidx)) ||
+          (rc2 = up(&fp.sidx, fh.sidx)) || (rc2 = up(&fp.red_idx, fh.red_idx)) || (rc2 = up(&fp.red_off, fh.red_off))) {
+        sigb_plan_destroy(plan);
+        return rc2;
+      }
+      fp.ok = true;
+    }
+  }
   // perm is stored per part at node_off (same offsets as the node tables)
   auto upload = [&](auto** dst, const auto& src) -> int {
     using E = typename std::remove_reference<decltype(src)>::type::value_type;
@@ -302,6 +349,12 @@ extern "C" int sigb_plan_destroy(sigb_plan* plan) {
   cudaFree(plan->d_nodeB);
   cudaFree(plan->d_perm);
   cudaFree(plan->d_lseg);
+  cudaFree(plan->frag.letter);
+  cudaFree(plan->frag.cidx);
+  cudaFree(plan->frag.eidx);
+  cudaFree(plan->frag.sidx);
+  cudaFree(plan->frag.red_idx);
+  cudaFree(plan->frag.red_off);
   delete plan;
   return SIGB_OK;
 }

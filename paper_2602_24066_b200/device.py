@@ -96,9 +96,17 @@ class Plan:
         self.prefix_closed = self.Wc == self.W
 
     @property
+    def kernel_kind(self) -> int:
+        """1 truncated, 2 fragment, 0 level-synchronous kernels (under the current policy)."""
+        return int(_lib.lib().sigb_plan_kernel_kind(self.handle))
+
+    @property
     def uses_truncated(self) -> bool:
-        """True when the register-resident truncated kernels serve this plan (current policy)."""
-        return int(_lib.lib().sigb_plan_kernel_kind(self.handle)) == 1
+        return self.kernel_kind == 1
+
+    @property
+    def uses_fragments(self) -> bool:
+        return self.kernel_kind == 2
 
     def __del__(self):
         h = getattr(self, "handle", None)

@@ -70,3 +70,32 @@ def test_error_codes_map_to_reference_hierarchy():
                             4: E.UnsupportedWordSetError}
     for cls in _lib._ERRORS.values():
         assert issubclass(cls, E.SigkitError)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_fragment_planner_covers_configs(name):
+    """The host-only fragment planner cuts every config's closure with full ownership coverage."""
+    import paper_2602_24066_b200 as sk
+    from tests.configs import build_wordset
+
+    ws = build_wordset(name, sk)
+    info = _lib.fragment_plan_info(ws.codes, ws.lengths, ws.d)
+    assert info["closure"] == len(ws)  # all five sets are prefix-closed
+    assert info["instantiated"] == 1
+    assert 1 <= info["NC"] <= 5 and info["fragments"] >= 1
+    assert info["ctas_per_path"] == -(-info["fragments"] // 128)
+
+
+def test_fragment_planner_random_sets():
+    import numpy as np
+
+    import paper_2602_24066_b200 as sk
+
+    rng = np.random.default_rng(0)
+    for _ in range(40):
+        d = int(rng.integers(1, 20))
+        words = {tuple(int(x) for x in rng.integers(0, d, int(rng.integers(1, 7)))) for _ in range(50)}
+        ws = sk.build_custom(sorted(words), d)
+        info = _lib.fragment_plan_info(ws.codes, ws.lengths, ws.d)
+        closure = {w[:k] for w in words for k in range(1, len(w) + 1)}
+        assert info["closure"] == len(closure)
