@@ -15,8 +15,9 @@ FragDev dev_of(const sigb_plan* p) {
   f.cidx = p->frag.cidx;
   f.eidx = p->frag.eidx;
   f.sidx = p->frag.sidx;
-  f.red_idx = p->frag.red_idx;
+  f.pos = p->frag.pos;
   f.red_off = p->frag.red_off;
+  f.pstride = p->frag.pstride;
   f.Fp = p->frag.Fp;
   f.cpp = p->frag.cpp;
   f.d = (int)p->d;
@@ -80,7 +81,7 @@ int bwd(const sigb_plan* p, const T* X, int64_t B, int64_t L, const T* S, int64_
   const int64_t chunk = bwd_chunk<T>(p, B, L);
   const size_t need = sizeof(T) * (size_t)chunk * cpp * M * d;
   if (!work || work_bytes < need) return fail(SIGB_ERR_DOMAIN, "backward workspace too small");
-  const size_t smem = sizeof(T) * bwd_smem_elems<NC, G, K>(d) + sizeof(unsigned short) * (size_t)p->frag.max_red + 16;
+  const size_t smem = sizeof(T) * bwd_smem_elems<NC, G, K>(d, p->frag.pstride);
   SIGB_CUDA_TRY(cudaFuncSetAttribute(frag_backward_kernel<T, NC, G, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
   T* partial = (T*)work;

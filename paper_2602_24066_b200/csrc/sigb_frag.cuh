@@ -132,9 +132,9 @@ struct FragDev {
   const int* cidx;              // [NS][Fp] closure index to read S (-1 empty, -2 identity)
   const int* eidx;              // [NS][Fp] emitted index in I (owner only) or -1
   const int* sidx;              // [NS][Fp] closure index to write state (owner only) or -1
-  const unsigned short* red_idx;  // per CTA-part CSR entries (slot * kTPB + tid), fixed order
-  const int* red_off;           // [cpp][d + 1] (offsets into red_idx, absolute)
-  int Fp, cpp, d;
+  const unsigned short* pos;    // [NGS][Fp] parking offset of the slot's gradient term (bwd)
+  const int* red_off;           // [cpp][d + 1] letter blocks of the parking buffer, float4 units
+  int Fp, cpp, d, pstride;
 };
 
 template <int NC, int G, int K>
@@ -223,10 +223,20 @@ __global__ void __launch_bounds__(kTPB) frag_forward_kernel(FragDev fd, const T*
   if (orow && include_empty && f == 0) orow[-1] = T(1);
 }
 
+// 16-byte aligned shared-memory load of four consecutive elements.
+__device__ __forceinline__ void load4(const float* p, float& a, float& b, float& c, float& d) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  a = v.x; b = v.y; c = v.z; d = v.w;
+}
+__device__ __forceinline__ void load4(const double* p, double& a, double& b, double& c, double& d) {
+  const double2 u = *reinterpret_cast<const double2*>(p);
+  const double2 v = *reinterpret_cast<const double2*>(p + 2);
+  a = u.x; b = u.y; c = v.x; d = v.y;
+}
+
 template <int NC, int G, int K>
-__host__ __device__ constexpr size_t bwd_smem_elems(int d) {
-  return (size_t)(kChunkF + 1) * d + (size_t)kChunkF * (d + 1) +
-         (size_t)kRedSteps * Shape<NC, G, K>::NGS * kTPB;
+__host__ __device__ constexpr size_t bwd_smem_elems(int d, int pstride) {
+  return (((size_t)(kChunkF + 1) * d + (size_t)kChunkF * (d + 1) + 3) / 4) * 4 + (size_t)kRedSteps * pstride;
 }
 
 // Backward over paths [b0, b0 + gridDim.x / cpp).  partial layout:
@@ -243,7 +253,8 @@ __global__ void __launch_bounds__(kTPB) frag_backward_kernel(FragDev fd, const T
   const int d = fd.d;
   T* Xs = reinterpret_cast<T*>(smem_raw);
   T* Dl = Xs + (kChunkF + 1) * d;
-  T* buf = Dl + kChunkF * (d + 1);  // [kRedSteps][NGS][kTPB]
+  // parking buffer [kRedSteps][pstride], letter-major (16-byte aligned)
+  T* buf = Xs + (((size_t)(kChunkF + 1) * d + (size_t)kChunkF * (d + 1) + 3) / 4) * 4;
   const int cip = (int)(blockIdx.x % fd.cpp);
   const int64_t bl = blockIdx.x / fd.cpp, b = b0 + bl;
   const int tid = threadIdx.x;
@@ -264,14 +275,15 @@ __global__ void __launch_bounds__(kTPB) frag_backward_kernel(FragDev fd, const T
       v = e >= 0 ? grow[e] : T(0);
     });
   }
-  // reduction geometry: rsplit lanes per letter (power of two <= 32)
-  int rsplit = 1;
-  while (rsplit * 2 <= 32 && rsplit * 2 * d <= kTPB) rsplit *= 2;
   const int* roff = fd.red_off + cip * (d + 1);
-  // this CTA-part's reduction list, staged once (u16 offsets into buf)
-  unsigned short* rl = reinterpret_cast<unsigned short*>(buf + (size_t)kRedSteps * NGS * kTPB);
-  const int rbase = roff[0];
-  for (int i = tid; i < roff[d] - rbase; i += kTPB) rl[i] = fd.red_idx[rbase + i];
+  int pos[NGS];
+#pragma unroll
+  for (int i = 0; i < NGS; ++i) pos[i] = fd.pos[(size_t)i * fd.Fp + f];
+  // zero the parking buffer once: letter blocks are padded to float4s that are never written
+  for (int i = tid; i < kRedSteps * fd.pstride; i += kTPB) buf[i] = T(0);
+  // reduction geometry: segments (parked step, letter), lps lanes per segment
+  int lps = 1;
+  while (lps * 2 <= 32 && lps * 2 * kRedSteps * d <= kTPB) lps *= 2;
   const T* Xb = X + b * L * d;
   T* pout = partial + (bl * fd.cpp + cip) * M * d;
   const int nchunks = (int)((M + kChunkF - 1) / kChunkF);
@@ -348,30 +360,42 @@ __global__ void __launch_bounds__(kTPB) frag_backward_kernel(FragDev fd, const T
             tbc[m] = (m >= lv) ? ((m == lv) ? in.dc[k] : in.dc[k] * rinv<T>(m - lv + 1)) * tbn[m] : T(0);
         }
       }
-      // (d) park this step's gradient terms (slot-major, conflict-free)
-      T* pb = buf + (size_t)nbuf * NGS * kTPB + tid;
+      // (d) park this step's gradient terms at their letter-major offsets
+      T* pb = buf + (size_t)nbuf * fd.pstride;
 #pragma unroll
-      for (int k = 0; k < NC; ++k) pb[k * kTPB] = gch[k];
+      for (int k = 0; k < NC; ++k) pb[pos[k]] = gch[k];
 #pragma unroll
-      for (int g = 0; g < G; ++g) pb[(NC + g) * kTPB] = gm[g];
+      for (int g = 0; g < G; ++g) pb[pos[NC + g]] = gm[g];
 #pragma unroll
-      for (int k = 0; k < K; ++k) pb[(NC + G + k) * kTPB] = gl[k];
+      for (int k = 0; k < K; ++k) pb[pos[NC + G + k]] = gl[k];
 #pragma unroll
-      for (int k = 0; k < K; ++k) pb[(NC + G + K + k) * kTPB] = ga[k];
+      for (int k = 0; k < K; ++k) pb[pos[NC + G + K + k]] = ga[k];
       ++nbuf;
       if (nbuf == kRedSteps || s == 0) {
         __syncthreads();
-        // per (parked step, letter): fixed-order CSR sum, rsplit lanes per letter
-        for (int r = 0; r < nbuf; ++r) {
-          const T* pr = buf + (size_t)r * NGS * kTPB;
-          const int jstep = j0 + s + (nbuf - 1 - r);  // buf[0] holds the latest (largest) step
-          for (int z0 = 0; z0 < d; z0 += kTPB / rsplit) {
-            const int z = z0 + tid / rsplit, sub = tid % rsplit;
-            T acc = T(0);
-            if (z < d)
-              for (int e = roff[z] - rbase + sub; e < roff[z + 1] - rbase; e += rsplit) acc += pr[rl[e]];
-            for (int o = rsplit / 2; o > 0; o /= 2) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (z < d && sub == 0) pout[(int64_t)jstep * d + z] = acc;
+        // each (parked step r, letter z) block is a contiguous run of float4s:
+        // lps lanes stride over it, then a fixed xor tree -- deterministic
+        for (int sg0 = 0; sg0 < kRedSteps * d; sg0 += kTPB / lps) {
+          const int sg = sg0 + tid / lps, sub = tid % lps;
+          const int r = sg / d, z = sg % d;
+          T acc = T(0);
+          if (sg < kRedSteps * d && r < nbuf) {
+            const T* pr = buf + (size_t)r * fd.pstride;
+            T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
+            for (int q = roff[z] + sub; q < roff[z + 1]; q += lps) {
+              T v0, v1, v2, v3;
+              load4(pr + 4 * q, v0, v1, v2, v3);
+              a0 += v0;
+              a1 += v1;
+              a2 += v2;
+              a3 += v3;
+            }
+            acc = (a0 + a1) + (a2 + a3);
+          }
+          for (int o = lps / 2; o > 0; o /= 2) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+          if (sg < kRedSteps * d && r < nbuf && sub == 0) {
+            const int jstep = j0 + s + (nbuf - 1 - r);  // buf[0] holds the latest (largest) step
+            pout[(int64_t)jstep * d + z] = acc;
           }
         }
         __syncthreads();

@@ -230,24 +230,37 @@ bool plan_fragments(const Trie& t, FragHost& out, std::string& why) {
       why = "internal: fragment cut missed closure node " + std::to_string(i);
       return false;
     }
-  // per CTA-part reduction lists: letter z <- (slot, tid) in ascending order
+  // per CTA-part letter-major parking layout for the backward's gradient terms:
+  // letter z's entries are contiguous (slot-major, then thread), each letter
+  // block padded to a float4; slots without a letter write to a trash float.
+  out.pos.assign((size_t)NGS * Fp, 0);
   out.red_off.assign((size_t)cpp * (t.d + 1), 0);
+  int pmax = 0;
   for (int c = 0; c < cpp; ++c) {
-    std::vector<std::vector<unsigned short>> by(t.d);
+    std::vector<int> cnt(t.d, 0);
     for (int slot = 0; slot < NGS; ++slot)
       for (int tid = 0; tid < TPB; ++tid) {
         const int z = out.letter[(size_t)slot * Fp + c * TPB + tid];
-        if (z < t.d) by[z].push_back((unsigned short)(slot * TPB + tid));
+        if (z < t.d) cnt[z]++;
       }
-    int cnt = 0;
-    for (int z = 0; z < t.d; ++z) {
-      out.red_off[(size_t)c * (t.d + 1) + z] = (int)out.red_idx.size();
-      out.red_idx.insert(out.red_idx.end(), by[z].begin(), by[z].end());
-      cnt += (int)by[z].size();
-    }
-    out.red_off[(size_t)c * (t.d + 1) + t.d] = (int)out.red_idx.size();
-    out.max_red = std::max(out.max_red, cnt);
+    std::vector<int> base(t.d + 1, 0);
+    for (int z = 0; z < t.d; ++z) base[z + 1] = base[z] + (cnt[z] + 3) / 4 * 4;
+    for (int z = 0; z <= t.d; ++z) out.red_off[(size_t)c * (t.d + 1) + z] = base[z] / 4;
+    const int trash = base[t.d];
+    std::vector<int> fill(base.begin(), base.end() - 1);
+    for (int slot = 0; slot < NGS; ++slot)
+      for (int tid = 0; tid < TPB; ++tid) {
+        const size_t i = (size_t)slot * Fp + c * TPB + tid;
+        const int z = out.letter[i];
+        out.pos[i] = (unsigned short)(z < t.d ? fill[z]++ : trash);
+      }
+    pmax = std::max(pmax, trash + 4);
   }
+  if (pmax > 65535) {
+    why = "fragment gradient buffer exceeds 16-bit offsets";
+    return false;
+  }
+  out.pstride = pmax;
   return true;
 }
 

@@ -76,9 +76,11 @@ struct FragHost {
   double cost = 0;           // estimated issue slots per path-step (forward)
   std::vector<unsigned char> letter;  // [NGS][Fp], d = none
   std::vector<int> cidx, eidx, sidx;  // [NS][Fp]
-  std::vector<unsigned short> red_idx;
-  std::vector<int> red_off;  // [cpp][d+1] absolute offsets into red_idx
-  int max_red = 0;           // largest per-CTA list (entries)
+  // backward gradient parking: slot (s, f) writes to pos[s][f] of a per-CTA
+  // letter-major buffer; letter z of CTA-part c owns float4s [off[c][z], off[c][z+1])
+  std::vector<unsigned short> pos;  // [NGS][Fp]
+  std::vector<int> red_off;         // [cpp][d+1] in float4 units
+  int pstride = 0;                  // floats per parked step (4-aligned, + trash)
 };
 
 // Builds the fragment decomposition of `t` for the best available template
@@ -87,10 +89,10 @@ bool plan_fragments(const Trie& t, FragHost& out, std::string& why);
 
 struct FragDevPlan {
   bool ok = false;
-  int NC = 0, G = 0, K = 0, F = 0, cpp = 0, Fp = 0, max_red = 0;
+  int NC = 0, G = 0, K = 0, F = 0, cpp = 0, Fp = 0, pstride = 0;
   unsigned char* letter = nullptr;
   int *cidx = nullptr, *eidx = nullptr, *sidx = nullptr;
-  unsigned short* red_idx = nullptr;
+  unsigned short* pos = nullptr;
   int* red_off = nullptr;
 };
 

@@ -303,7 +303,7 @@ extern "C" int sigb_plan_create(const uint64_t* codes, const int64_t* lengths, i
     if (plan_fragments(t, fh, why) && frag::supported(fh.NC, fh.G, fh.K)) {
       FragDevPlan& fp = plan->frag;
       fp.NC = fh.NC; fp.G = fh.G; fp.K = fh.K; fp.F = fh.F; fp.cpp = fh.cpp; fp.Fp = fh.Fp;
-      fp.max_red = fh.max_red;
+      fp.pstride = fh.pstride;
       int rc2;
       auto up = [&](auto** dst, const auto& src) -> int {
         using E = typename std::remove_reference<decltype(src)>::type::value_type;
@@ -313,7 +313,7 @@ extern "C" int sigb_plan_create(const uint64_t* codes, const int64_t* lengths, i
         return SIGB_OK;
       };
       if ((rc2 = up(&fp.letter, fh.letter)) || (rc2 = up(&fp.cidx, fh.cidx)) || (rc2 = up(&fp.eidx, fh.eidx)) ||
-          (rc2 = up(&fp.sidx, fh.sidx)) || (rc2 = up(&fp.red_idx, fh.red_idx)) || (rc2 = up(&fp.red_off, fh.red_off))) {
+          (rc2 = up(&fp.sidx, fh.sidx)) || (rc2 = up(&fp.pos, fh.pos)) || (rc2 = up(&fp.red_off, fh.red_off))) {
         sigb_plan_destroy(plan);
         return rc2;
       }
@@ -353,7 +353,7 @@ extern "C" int sigb_plan_destroy(sigb_plan* plan) {
   cudaFree(plan->frag.cidx);
   cudaFree(plan->frag.eidx);
   cudaFree(plan->frag.sidx);
-  cudaFree(plan->frag.red_idx);
+  cudaFree(plan->frag.pos);
   cudaFree(plan->frag.red_off);
   delete plan;
   return SIGB_OK;

@@ -16,7 +16,7 @@ int fwd(const T* X, int64_t B, int64_t L, T* out, int64_t out_ld, int64_t out_co
   using C = Cfg<D, N, G>;
   const int64_t grid = C::CPP > 1 ? B * C::CPP : (B + C::PPC - 1) / C::PPC;
   if (grid == 0) return SIGB_OK;
-  constexpr size_t smem = sizeof(T) * ((size_t)C::PPC * (kChunkT + 1) * D + (size_t)C::PPC * kChunkT * D);
+  constexpr size_t smem = 0;  // static shared memory only
   count_launch();
   timing_begin(0, stream);
   trunc_forward_kernel<T, D, N, G><<<(unsigned)grid, C::THREADS, smem, stream>>>(X, B, L, out, out_ld, out_col0,
@@ -94,21 +94,23 @@ int bwd(const T* X, int64_t B, int64_t L, const T* S, int64_t s_ld, int64_t s_co
   return SIGB_OK;
 }
 
-// (D, N) -> G instantiations.  G = D when the fragment fits the register
-// budget of the backward, else the largest power of two that does.
+// (D, N) -> (G forward, G backward).  The forward and backward kernels share
+// only the output layout, so each picks its own fragment width: G = D where
+// the fragment fits the register budget, smaller where occupancy pays more
+// (d=8, N=5 backward: 168 registers at G=8 leave 8 warps per SM).
 #define SIGB_TRUNC_CASES(X) \
-  X(4, 4, 4)                \
-  X(4, 5, 4)                \
-  X(4, 6, 4)                \
-  X(8, 4, 8)                \
-  X(8, 5, 8)                \
-  X(16, 3, 4)               \
-  X(16, 4, 4)
+  X(4, 4, 4, 4)             \
+  X(4, 5, 4, 4)             \
+  X(4, 6, 4, 4)             \
+  X(8, 4, 8, 8)             \
+  X(8, 5, 8, 4)             \
+  X(16, 3, 4, 4)            \
+  X(16, 4, 4, 4)
 
 }  // namespace
 
 bool supported(int64_t d, int depth) {
-#define X(D_, N_, G_) \
+#define X(D_, N_, GF_, GB_) \
   if (d == D_ && depth == N_) return true;
   SIGB_TRUNC_CASES(X)
 #undef X
@@ -117,12 +119,12 @@ bool supported(int64_t d, int depth) {
 
 int forward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L, void* out, int64_t out_ld,
             int64_t out_col0, int include_empty, cudaStream_t stream) {
-#define X(D_, N_, G_)                                                                                      \
+#define X(D_, N_, GF_, GB_)                                                                                \
   if (d == D_ && depth == N_) {                                                                            \
     if (dtype == SIGB_F32)                                                                                 \
-      return fwd<float, D_, N_, G_>((const float*)X, B, L, (float*)out, out_ld, out_col0, include_empty,   \
+      return fwd<float, D_, N_, GF_>((const float*)X, B, L, (float*)out, out_ld, out_col0, include_empty,   \
                                     stream);                                                               \
-    return fwd<double, D_, N_, G_>((const double*)X, B, L, (double*)out, out_ld, out_col0, include_empty,  \
+    return fwd<double, D_, N_, GF_>((const double*)X, B, L, (double*)out, out_ld, out_col0, include_empty,  \
                                    stream);                                                                \
   }
   SIGB_TRUNC_CASES(X)
@@ -131,9 +133,9 @@ int forward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L
 }
 
 size_t backward_workspace(int dtype, int64_t d, int depth, int64_t B, int64_t L) {
-#define X(D_, N_, G_)                                                                             \
+#define X(D_, N_, GF_, GB_)                                                                       \
   if (d == D_ && depth == N_)                                                                     \
-    return dtype == SIGB_F32 ? bwd_workspace<float, D_, N_, G_>(B, L) : bwd_workspace<double, D_, N_, G_>(B, L);
+    return dtype == SIGB_F32 ? bwd_workspace<float, D_, N_, GB_>(B, L) : bwd_workspace<double, D_, N_, GB_>(B, L);
   SIGB_TRUNC_CASES(X)
 #undef X
   return 0;
@@ -142,12 +144,12 @@ size_t backward_workspace(int dtype, int64_t d, int depth, int64_t B, int64_t L)
 int backward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L, const void* S, int64_t s_ld,
              int64_t s_col0, const void* g, int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, void* dX,
              void* dinc, cudaStream_t stream) {
-#define X(D_, N_, G_)                                                                                             \
+#define X(D_, N_, GF_, GB_)                                                                                       \
   if (d == D_ && depth == N_) {                                                                                   \
     if (dtype == SIGB_F32)                                                                                        \
-      return bwd<float, D_, N_, G_>((const float*)X, B, L, (const float*)S, s_ld, s_col0, (const float*)g, g_ld,  \
+      return bwd<float, D_, N_, GB_>((const float*)X, B, L, (const float*)S, s_ld, s_col0, (const float*)g, g_ld,  \
                                     g_col0, work, work_bytes, (float*)dX, (float*)dinc, stream);                  \
-    return bwd<double, D_, N_, G_>((const double*)X, B, L, (const double*)S, s_ld, s_col0, (const double*)g,     \
+    return bwd<double, D_, N_, GB_>((const double*)X, B, L, (const double*)S, s_ld, s_col0, (const double*)g,     \
                                    g_ld, g_col0, work, work_bytes, (double*)dX, (double*)dinc, stream);           \
   }
   SIGB_TRUNC_CASES(X)

@@ -131,6 +131,35 @@ __device__ __forceinline__ void stage_increments(const T* __restrict__ X, int64_
   __syncthreads();
 }
 
+// Register prefetch of the samples of the next chunk (forward): issued before
+// the current chunk's steps so the global-load latency hides behind them.
+template <typename T, int D, int PPC, int CH, int NT>
+struct Prefetch {
+  static constexpr int PF = (PPC * (CH + 1) * D + NT - 1) / NT;
+  T v[PF];
+  __device__ __forceinline__ void load(const T* __restrict__ X, int64_t b_first, int64_t B, int64_t L, int64_t j0,
+                                       int cs) {
+    const int rows = cs + 1;
+#pragma unroll
+    for (int k = 0; k < PF; ++k) {
+      const int i = threadIdx.x + k * NT;
+      const int pc = i / (rows * D), r = i % (rows * D);
+      const int64_t b = b_first + pc;
+      v[k] = (pc < PPC && b < B) ? X[(b * L + j0) * D + r] : T(0);
+    }
+  }
+  // Xs[pc][r] layout with row pitch (CH + 1) * D, as stage_increments.
+  __device__ __forceinline__ void commit(T* __restrict__ Xs, int cs) const {
+    const int rows = cs + 1;
+#pragma unroll
+    for (int k = 0; k < PF; ++k) {
+      const int i = threadIdx.x + k * NT;
+      const int pc = i / (rows * D), r = i % (rows * D);
+      if (pc < PPC) Xs[pc * (CH + 1) * D + r] = v[k];
+    }
+  }
+};
+
 template <typename T, int D>
 __device__ __forceinline__ void load_row(const T* __restrict__ src, T (&v)[D], T sign) {
   if constexpr (sizeof(T) == 4 && D % 4 == 0) {
@@ -218,13 +247,16 @@ __device__ __forceinline__ void chen_step(State<T, D, N, G>& st, const StepIncr<
   }
 }
 
+constexpr int kChunkFwd = 32;  // forward steps per staged chunk
+
 template <typename T, int D, int N, int G>
 __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
     trunc_forward_kernel(const T* __restrict__ X, int64_t B, int64_t L, T* __restrict__ out, int64_t out_ld,
                          int64_t out_col0, int include_empty) {
   using C = Cfg<D, N, G>;
-  __shared__ __align__(16) T Xs[C::PPC * (kChunkT + 1) * D];
-  __shared__ __align__(16) T Dl[C::PPC * kChunkT * D];
+  constexpr int CH = kChunkFwd;
+  __shared__ __align__(16) T Xs[C::PPC * (CH + 1) * D];
+  __shared__ __align__(16) T Dl[C::PPC * CH * D];
   const Frag<D, N, G> f(blockIdx.x, threadIdx.x);
   const int64_t b_first = C::CPP > 1 ? f.b : (int64_t)blockIdx.x * C::PPC;
   State<T, D, N, G> st;
@@ -237,10 +269,21 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
     for (int z = 0; z < D; ++z) st.leaf[g][z] = T(0);
   }
   const int64_t M = L - 1;
-  for (int64_t j0 = 0; j0 < M; j0 += kChunkT) {
-    const int cs = (int)(M - j0 < kChunkT ? M - j0 : kChunkT);
-    stage_increments<T, D, C::PPC>(X, b_first, B, L, (int)j0, cs, Xs, Dl);
-    const T* rows = Dl + f.pc * kChunkT * D;
+  Prefetch<T, D, C::PPC, CH, C::THREADS> pf;
+  if (M > 0) pf.load(X, b_first, B, L, 0, (int)(M < CH ? M : CH));
+  for (int64_t j0 = 0; j0 < M; j0 += CH) {
+    const int cs = (int)(M - j0 < CH ? M - j0 : CH);
+    pf.commit(Xs, cs);
+    __syncthreads();  // samples visible; every thread is past the previous chunk's steps
+    for (int i = threadIdx.x; i < C::PPC * cs * D; i += blockDim.x) {
+      const int pc = i / (cs * D), r = i % (cs * D);
+      const T* xs = Xs + pc * (CH + 1) * D;
+      Dl[pc * CH * D + r] = xs[r + D] - xs[r];
+    }
+    __syncthreads();
+    const int64_t j1 = j0 + CH;
+    if (j1 < M) pf.load(X, b_first, B, L, j1, (int)(M - j1 < CH ? M - j1 : CH));  // in flight during the steps
+    const T* rows = Dl + f.pc * CH * D;
 #pragma unroll 1
     for (int s = 0; s < cs; ++s) {
       StepIncr<T, D, N, G> in;

@@ -21,7 +21,7 @@ import torch
 
 from .device import resolve_device
 from .exceptions import DomainError, ShapeError
-from .signature import PathBatch, _is_tensor, as_path_batch, forward_tensor, to_device
+from .signature import PathBatch, _is_tensor, as_path_batch, forward_tensor, to_device, to_host
 from .wordcodes import Word, decode_word
 from .wordset import WordSet
 
@@ -157,5 +157,5 @@ def signature_backward(paths, ws: WordSet, upstream, threads: int | None = None,
     up_words = up[:, g_col0:]
     if is_t:
         return GradBatch(upstream=up_words, increment_grads=dinc, path_grads=dX)
-    return GradBatch(upstream=np.ascontiguousarray(up_words), increment_grads=dinc.cpu().numpy(),
-                     path_grads=dX.cpu().numpy())
+    return GradBatch(upstream=np.ascontiguousarray(up_words), increment_grads=to_host(dinc),
+                     path_grads=to_host(dX))

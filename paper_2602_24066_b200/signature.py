@@ -194,6 +194,17 @@ def to_device(samples, device) -> torch.Tensor:
     return host.to(device, non_blocking=True)
 
 
+def to_host(t: torch.Tensor) -> np.ndarray:
+    """Device tensor -> numpy.  Large results land in pinned host memory (torch's caching
+    host allocator), so the D2H copy runs at full PCIe speed instead of through a
+    pageable bounce buffer; the returned array keeps the pinned block alive."""
+    if t.is_cuda and t.numel() * t.element_size() >= (1 << 20):
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t)
+        return h.numpy()
+    return t.cpu().numpy()
+
+
 def forward_tensor(X: torch.Tensor, ws: WordSet, want_state: bool = False):
     """(out (B, width), closure state or None) for a CUDA tensor X (B, L, d)."""
     plan = ws.plan(X.device)
@@ -221,7 +232,7 @@ def signature_forward(paths, ws: WordSet, threads: int | None = None) -> Coeffic
     dev = resolve_device()
     X = to_device(paths.samples, dev)
     out, _ = forward_tensor(X, ws)
-    return CoefficientBatch(ws, out.cpu().numpy())
+    return CoefficientBatch(ws, to_host(out))
 
 
 def signature_windows(paths, ws: WordSet, windows, threads: int | None = None) -> list[CoefficientBatch]:
@@ -243,5 +254,5 @@ def signature_windows(paths, ws: WordSet, windows, threads: int | None = None) -
         v = out[:, k, :]
         if ws.include_empty:
             v = torch.cat([torch.ones((paths.B, 1), dtype=X.dtype, device=dev), v], dim=1)
-        res.append(CoefficientBatch(ws, v if is_t else v.cpu().numpy()))
+        res.append(CoefficientBatch(ws, v if is_t else to_host(v.contiguous())))
     return res
