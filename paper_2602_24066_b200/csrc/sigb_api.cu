@@ -231,11 +231,12 @@ extern "C" int sigb_forward(const sigb_plan* plan, int dtype, const void* d_X, i
   if (rc) return rc;
   if (include_empty && out_col0 < 1) return fail(SIGB_ERR_SHAPE, "include_empty needs out_col0 >= 1");
   if (use_trunc(plan)) {
-    return trunc::forward(dtype, plan->d, plan->trunc_depth, d_X, B, L, d_out, out_ld, out_col0, include_empty,
+    return trunc::forward(dtype, plan->d, plan->trunc_depth, d_X, B, L, nullptr, 1, d_out, out_ld, out_col0, include_empty,
                           (cudaStream_t)stream);
   }
   if (use_frag(plan))
-    return frag::forward(plan, dtype, d_X, B, L, d_out, out_ld, out_col0, include_empty, d_state, (cudaStream_t)stream);
+    return frag::forward(plan, dtype, d_X, B, L, nullptr, 1, d_out, out_ld, out_col0, include_empty, d_state,
+                         (cudaStream_t)stream);
   if (dtype == SIGB_F32)
     return forward_t<float>(plan, d_X, B, L, nullptr, 1, d_out, out_ld, out_col0, include_empty, d_state, nullptr, 0,
                             0, (cudaStream_t)stream);
@@ -248,6 +249,12 @@ extern "C" int sigb_windows(const sigb_plan* plan, int dtype, const void* d_X, i
   int rc = check_common(plan, dtype, B, L);
   if (rc) return rc;
   if (K < 1 || !d_bounds) return fail(SIGB_ERR_DOMAIN, "need at least one window");
+  // windows = B*K virtual paths over the same register-resident kernels as sigb_forward
+  if (use_trunc(plan))
+    return trunc::forward(dtype, plan->d, plan->trunc_depth, d_X, B * K, L, d_bounds, K, d_out, plan->W, 0, 0,
+                          (cudaStream_t)stream);
+  if (use_frag(plan))
+    return frag::forward(plan, dtype, d_X, B * K, L, d_bounds, K, d_out, plan->W, 0, 0, nullptr, (cudaStream_t)stream);
   if (dtype == SIGB_F32)
     return forward_t<float>(plan, d_X, B, L, d_bounds, K, d_out, plan->W, 0, 0, nullptr, nullptr, 0, 0,
                             (cudaStream_t)stream);

@@ -25,8 +25,8 @@ FragDev dev_of(const sigb_plan* p) {
 }
 
 template <typename T, int NC, int G, int K>
-int fwd(const sigb_plan* p, const T* X, int64_t B, int64_t L, T* out, int64_t out_ld, int64_t out_col0,
-        int include_empty, T* state, cudaStream_t stream) {
+int fwd(const sigb_plan* p, const T* X, int64_t B, int64_t L, const int64_t* bounds, int64_t nwin, T* out,
+        int64_t out_ld, int64_t out_col0, int include_empty, T* state, cudaStream_t stream) {
   const int d = (int)p->d;
   const int64_t grid = B * p->frag.cpp;
   if (grid == 0) return SIGB_OK;
@@ -36,8 +36,8 @@ int fwd(const sigb_plan* p, const T* X, int64_t B, int64_t L, T* out, int64_t ou
                                        (int)smem));
   count_launch();
   timing_begin(0, stream);
-  frag_forward_kernel<T, NC, G, K><<<(unsigned)grid, kTPB, smem, stream>>>(dev_of(p), X, L, out, out_ld, out_col0,
-                                                                            include_empty, state, p->Wc);
+  frag_forward_kernel<T, NC, G, K><<<(unsigned)grid, kTPB, smem, stream>>>(dev_of(p), X, L, bounds, nwin, out, out_ld,
+                                                                            out_col0, include_empty, state, p->Wc);
   timing_end(0, stream);
   SIGB_CUDA_TRY(cudaGetLastError());
   return SIGB_OK;
@@ -113,16 +113,16 @@ bool supported(int NC, int G, int K) {
   return false;
 }
 
-int forward(const sigb_plan* p, int dtype, const void* Xv, int64_t B, int64_t L, void* out, int64_t out_ld,
-            int64_t out_col0, int include_empty, void* state, cudaStream_t stream) {
+int forward(const sigb_plan* p, int dtype, const void* Xv, int64_t B, int64_t L, const int64_t* bounds, int64_t nwin,
+            void* out, int64_t out_ld, int64_t out_col0, int include_empty, void* state, cudaStream_t stream) {
   const int NC = p->frag.NC, G = p->frag.G, K = p->frag.K;
 #define X(a, b, c)                                                                                               \
   if (NC == a && G == b && K == c) {                                                                             \
     if (dtype == SIGB_F32)                                                                                       \
-      return fwd<float, a, b, c>(p, (const float*)Xv, B, L, (float*)out, out_ld, out_col0, include_empty,        \
-                                 (float*)state, stream);                                                         \
-    return fwd<double, a, b, c>(p, (const double*)Xv, B, L, (double*)out, out_ld, out_col0, include_empty,       \
-                                (double*)state, stream);                                                         \
+      return fwd<float, a, b, c>(p, (const float*)Xv, B, L, bounds, nwin, (float*)out, out_ld, out_col0,            \
+                                 include_empty, (float*)state, stream);                                          \
+    return fwd<double, a, b, c>(p, (const double*)Xv, B, L, bounds, nwin, (double*)out, out_ld, out_col0,           \
+                                include_empty, (double*)state, stream);                                          \
   }
   SIGB_FRAG_CASES(X)
 #undef X

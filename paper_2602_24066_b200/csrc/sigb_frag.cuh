@@ -186,19 +186,25 @@ __device__ __forceinline__ void stage(const T* __restrict__ Xb, int d, int j0, i
 
 template <typename T, int NC, int G, int K>
 __global__ void __launch_bounds__(kTPB) frag_forward_kernel(FragDev fd, const T* __restrict__ X, int64_t L,
+                                                            const int64_t* __restrict__ bounds, int64_t nwin,
                                                             T* __restrict__ out, int64_t out_ld, int64_t out_col0,
                                                             int include_empty, T* __restrict__ state, int64_t Wc) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Xs = reinterpret_cast<T*>(smem_raw);
   T* Dl = Xs + (kChunkF + 1) * fd.d;
-  const int64_t b = blockIdx.x / fd.cpp;
+  const int64_t b = blockIdx.x / fd.cpp;  // virtual path: window b % nwin of path b / nwin
   const int f = (int)(blockIdx.x % fd.cpp) * kTPB + threadIdx.x;
   Letters<NC, G, K> lt;
   load_letters<NC, G, K>(fd, f, lt);
   FState<T, NC, G, K> st;
   for_slots<T, NC, G, K>(st, [&](int i, T& v) { v = fd.cidx[(size_t)i * fd.Fp + f] == -2 ? T(1) : T(0); });
-  const int64_t M = L - 1;
+  int64_t M = L - 1;
   const T* Xb = X + b * L * fd.d;
+  if (bounds) {
+    const int64_t k = b % nwin, lo = bounds[2 * k];
+    M = bounds[2 * k + 1] - lo;
+    Xb = X + ((b / nwin) * L + lo) * fd.d;
+  }
   for (int64_t j0 = 0; j0 < M; j0 += kChunkF) {
     const int cs = (int)(M - j0 < kChunkF ? M - j0 : kChunkF);
     stage<T>(Xb, fd.d, (int)j0, cs, Xs, Dl);

@@ -142,8 +142,9 @@ void timing_begin(int which, cudaStream_t stream);
 void timing_end(int which, cudaStream_t stream);
 namespace frag {
 bool supported(int NC, int G, int K);
-int forward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, void* out, int64_t out_ld,
-            int64_t out_col0, int include_empty, void* state, cudaStream_t stream);
+// bounds (K, 2) / K: windowed forward over B*K virtual paths (bounds NULL, K 1: whole paths)
+int forward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, const int64_t* bounds, int64_t K,
+            void* out, int64_t out_ld, int64_t out_col0, int include_empty, void* state, cudaStream_t stream);
 size_t backward_workspace(const sigb_plan* p, int dtype, int64_t B, int64_t L);
 int backward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, const void* S, int64_t s_ld,
              int64_t s_col0, const void* g, int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, void* dX,
@@ -151,8 +152,8 @@ int backward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L,
 }  // namespace frag
 namespace trunc {
 bool supported(int64_t d, int depth);
-int forward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L, void* out, int64_t out_ld,
-            int64_t out_col0, int include_empty, cudaStream_t stream);
+int forward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L, const int64_t* bounds, int64_t K,
+            void* out, int64_t out_ld, int64_t out_col0, int include_empty, cudaStream_t stream);
 size_t backward_workspace(int dtype, int64_t d, int depth, int64_t B, int64_t L);
 int backward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L, const void* S, int64_t s_ld,
              int64_t s_col0, const void* g, int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, void* dX,

@@ -11,16 +11,16 @@ namespace {
 constexpr size_t kPartialBudget = size_t(8) << 30;  // bytes of per-part gradient partials per chunk
 
 template <typename T, int D, int N, int G>
-int fwd(const T* X, int64_t B, int64_t L, T* out, int64_t out_ld, int64_t out_col0, int include_empty,
-        cudaStream_t stream) {
+int fwd(const T* X, int64_t B, int64_t L, const int64_t* bounds, int64_t K, T* out, int64_t out_ld, int64_t out_col0,
+        int include_empty, cudaStream_t stream) {
   using C = Cfg<D, N, G>;
   const int64_t grid = C::CPP > 1 ? B * C::CPP : (B + C::PPC - 1) / C::PPC;
   if (grid == 0) return SIGB_OK;
   constexpr size_t smem = 0;  // static shared memory only
   count_launch();
   timing_begin(0, stream);
-  trunc_forward_kernel<T, D, N, G><<<(unsigned)grid, C::THREADS, smem, stream>>>(X, B, L, out, out_ld, out_col0,
-                                                                                include_empty);
+  trunc_forward_kernel<T, D, N, G><<<(unsigned)grid, C::THREADS, smem, stream>>>(X, B, L, bounds, K, out, out_ld,
+                                                                                out_col0, include_empty);
   timing_end(0, stream);
   SIGB_CUDA_TRY(cudaGetLastError());
   return SIGB_OK;
@@ -117,15 +117,15 @@ bool supported(int64_t d, int depth) {
   return false;
 }
 
-int forward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L, void* out, int64_t out_ld,
-            int64_t out_col0, int include_empty, cudaStream_t stream) {
+int forward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L, const int64_t* bounds, int64_t K,
+            void* out, int64_t out_ld, int64_t out_col0, int include_empty, cudaStream_t stream) {
 #define X(D_, N_, GF_, GB_)                                                                                \
   if (d == D_ && depth == N_) {                                                                            \
     if (dtype == SIGB_F32)                                                                                 \
-      return fwd<float, D_, N_, GF_>((const float*)X, B, L, (float*)out, out_ld, out_col0, include_empty,   \
-                                    stream);                                                               \
-    return fwd<double, D_, N_, GF_>((const double*)X, B, L, (double*)out, out_ld, out_col0, include_empty,  \
-                                   stream);                                                                \
+      return fwd<float, D_, N_, GF_>((const float*)X, B, L, bounds, K, (float*)out, out_ld, out_col0,       \
+                                     include_empty, stream);                                               \
+    return fwd<double, D_, N_, GF_>((const double*)X, B, L, bounds, K, (double*)out, out_ld, out_col0,     \
+                                    include_empty, stream);                                                \
   }
   SIGB_TRUNC_CASES(X)
 #undef X

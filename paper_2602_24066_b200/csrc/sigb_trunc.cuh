@@ -137,15 +137,29 @@ template <typename T, int D, int PPC, int CH, int NT>
 struct Prefetch {
   static constexpr int PF = (PPC * (CH + 1) * D + NT - 1) / NT;
   T v[PF];
-  __device__ __forceinline__ void load(const T* __restrict__ X, int64_t b_first, int64_t B, int64_t L, int64_t j0,
-                                       int cs) {
+  // Virtual path v = b_first + pc is window (v % K) of path v / K (K = 1, bounds
+  // = NULL: the whole path).  Samples past the window's end are clamped to its
+  // last sample, so their increments are exactly zero and the Chen step a no-op.
+  __device__ __forceinline__ void load(const T* __restrict__ X, int64_t b_first, int64_t B, int64_t L,
+                                       const int64_t* __restrict__ bounds, int64_t K, int64_t t0, int cs) {
     const int rows = cs + 1;
 #pragma unroll
     for (int k = 0; k < PF; ++k) {
       const int i = threadIdx.x + k * NT;
       const int pc = i / (rows * D), r = i % (rows * D);
-      const int64_t b = b_first + pc;
-      v[k] = (pc < PPC && b < B) ? X[(b * L + j0) * D + r] : T(0);
+      const int64_t vp = b_first + pc;
+      T val = T(0);
+      if (pc < PPC && vp < B) {
+        int64_t b = vp, lo = 0, len = L - 1;
+        if (bounds) {
+          b = vp / K;
+          lo = bounds[2 * (vp % K)];
+          len = bounds[2 * (vp % K) + 1] - lo;
+        }
+        const int64_t t = t0 + r / D;
+        val = X[(b * L + lo + (t < len ? t : len)) * D + r % D];
+      }
+      v[k] = val;
     }
   }
   // Xs[pc][r] layout with row pitch (CH + 1) * D, as stage_increments.
@@ -251,8 +265,8 @@ constexpr int kChunkFwd = 32;  // forward steps per staged chunk
 
 template <typename T, int D, int N, int G>
 __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
-    trunc_forward_kernel(const T* __restrict__ X, int64_t B, int64_t L, T* __restrict__ out, int64_t out_ld,
-                         int64_t out_col0, int include_empty) {
+    trunc_forward_kernel(const T* __restrict__ X, int64_t B, int64_t L, const int64_t* __restrict__ bounds,
+                         int64_t K, T* __restrict__ out, int64_t out_ld, int64_t out_col0, int include_empty) {
   using C = Cfg<D, N, G>;
   constexpr int CH = kChunkFwd;
   __shared__ __align__(16) T Xs[C::PPC * (CH + 1) * D];
@@ -268,9 +282,17 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
 #pragma unroll
     for (int z = 0; z < D; ++z) st.leaf[g][z] = T(0);
   }
-  const int64_t M = L - 1;
+  // steps of this CTA: the longest window among its (virtual) paths
+  int64_t M = L - 1;
+  if (bounds) {
+    M = 0;
+    for (int pc = 0; pc < C::PPC; ++pc) {
+      const int64_t vp = b_first + pc;
+      if (vp < B) M = max(M, bounds[2 * (vp % K) + 1] - bounds[2 * (vp % K)]);
+    }
+  }
   Prefetch<T, D, C::PPC, CH, C::THREADS> pf;
-  if (M > 0) pf.load(X, b_first, B, L, 0, (int)(M < CH ? M : CH));
+  if (M > 0) pf.load(X, b_first, B, L, bounds, K, 0, (int)(M < CH ? M : CH));
   for (int64_t j0 = 0; j0 < M; j0 += CH) {
     const int cs = (int)(M - j0 < CH ? M - j0 : CH);
     pf.commit(Xs, cs);
@@ -282,7 +304,7 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
     }
     __syncthreads();
     const int64_t j1 = j0 + CH;
-    if (j1 < M) pf.load(X, b_first, B, L, j1, (int)(M - j1 < CH ? M - j1 : CH));  // in flight during the steps
+    if (j1 < M) pf.load(X, b_first, B, L, bounds, K, j1, (int)(M - j1 < CH ? M - j1 : CH));  // in flight during steps
     const T* rows = Dl + f.pc * CH * D;
 #pragma unroll 1
     for (int s = 0; s < cs; ++s) {
@@ -340,10 +362,13 @@ struct RedGeom {
   using C = Cfg<D, N, G>;
   static constexpr int GPW = C::RW / C::Q > 0 ? C::RW / C::Q : 1;  // gp groups per reduction group
   static constexpr int RGW = 32 / C::RW;                              // reduction groups per warp
+  static constexpr int NE = C::NW * RGW * GPW * (C::NC > 0 ? C::NC : 1);  // chain terms per parked step
+  static constexpr int NKEY = C::PPC * D;                                 // (path slot, letter)
   template <typename T>
   static constexpr size_t smem_bytes() {
     return sizeof(T) * ((size_t)C::PPC * (kChunkT + 1) * D + (size_t)C::PPC * kChunkT * D +
-                        (size_t)C::NW * RGW * kChunkT * D + (size_t)C::NW * RGW * kChunkT * GPW * (C::NC > 0 ? C::NC : 1));
+                        (size_t)C::NW * RGW * kChunkT * D + (size_t)C::NW * RGW * kChunkT * GPW * (C::NC > 0 ? C::NC : 1)) +
+           sizeof(int) * (NKEY + 1) + sizeof(unsigned short) * NE;
   }
 };
 
@@ -365,6 +390,11 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
   T(*red_leaf)[RG::RGW][kChunkT][D] = reinterpret_cast<T(*)[RG::RGW][kChunkT][D]>(Dl + C::PPC * kChunkT * D);
   T(*red_chain)[RG::RGW][kChunkT][RG::GPW][NCc] =
       reinterpret_cast<T(*)[RG::RGW][kChunkT][RG::GPW][NCc]>(Dl + C::PPC * kChunkT * D + C::NW * RG::RGW * kChunkT * D);
+  // per-(path slot, letter) lists of this CTA's parked chain terms, built once:
+  // replaces a per-element scan of every chain term in the chunk epilogue
+  int* key_off = reinterpret_cast<int*>(reinterpret_cast<T*>(Dl + C::PPC * kChunkT * D + C::NW * RG::RGW * kChunkT * D) +
+                                        C::NW * RG::RGW * kChunkT * RG::GPW * NCc);
+  unsigned short* key_idx = reinterpret_cast<unsigned short*>(key_off + RG::NKEY + 1);
   const int64_t cta = blockIdx.x + (C::CPP > 1 ? b0 * C::CPP : b0 / C::PPC);
   const Frag<D, N, G> f(cta, threadIdx.x);
   const int64_t b_first = C::CPP > 1 ? f.b : cta * C::PPC;
@@ -391,6 +421,28 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
         st.leaf[g][z] = live ? srow[f.leaf_index(g, z)] : T(0);
         lam.leaf[g][z] = live ? grow[f.leaf_index(g, z)] : T(0);
       }
+    }
+  }
+  if (threadIdx.x == 0) {
+    // entry e = ((w * RGW + r) * GPW + gg) * NCc + k; its letter is digit k of its grand-parent
+    auto key_of = [&](int e) {
+      const int k = e % NCc, gg = (e / NCc) % RG::GPW, wr = e / (NCc * RG::GPW);
+      const int first_thread = (wr / RG::RGW) * 32 + (wr % RG::RGW) * C::RW;
+      const int pc = C::CPP > 1 ? 0 : first_thread / C::TPP;
+      const int tt = (C::CPP > 1 ? f.cip * kThreadsT : 0) + (first_thread % C::TPP) + gg * C::Q;
+      int code = tt / C::Q;
+      for (int q = NC - 1; q > k; --q) code /= D;
+      return pc * D + code % D;
+    };
+    for (int i = 0; i <= RG::NKEY; ++i) key_off[i] = 0;
+    for (int e = 0; e < RG::NE; ++e) key_off[key_of(e) + 1]++;
+    for (int i = 0; i < RG::NKEY; ++i) key_off[i + 1] += key_off[i];
+    int fill[RG::NKEY > 0 ? RG::NKEY : 1];
+    for (int i = 0; i < RG::NKEY; ++i) fill[i] = key_off[i];
+    for (int e = 0; e < RG::NE; ++e) {
+      const int k = e % NCc, gg = (e / NCc) % RG::GPW, wr = e / (NCc * RG::GPW);
+      // offset of red_chain[w][r][0][gg][k]
+      key_idx[fill[key_of(e)]++] = (unsigned short)((wr * kChunkT * RG::GPW + gg) * NCc + k);
     }
   }
   const int nchunks = (int)((M + kChunkT - 1) / kChunkT);
@@ -500,26 +552,21 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
       const int64_t b = b_first + pc;
       if (b >= B) continue;
       T acc = T(0);
-      // warps / reduction groups belonging to path slot pc
+      // leaf letters: the warps / reduction groups belonging to path slot pc
 #pragma unroll 1
       for (int w = 0; w < C::NW; ++w) {
-#pragma unroll 1
+#pragma unroll
         for (int r = 0; r < RG::RGW; ++r) {
           const int first_thread = w * 32 + r * C::RW;
           if (first_thread / C::TPP != pc && C::CPP == 1) continue;
           acc += red_leaf[w][r][s][z];
-#pragma unroll 1
-          for (int gg = 0; gg < RG::GPW; ++gg) {
-            const int tt = (C::CPP > 1 ? f.cip * kThreadsT : 0) + (first_thread % C::TPP) + gg * C::Q;
-            int code = tt / C::Q;
-#pragma unroll
-            for (int k = NC - 1; k >= 0; --k) {
-              if (code % D == z) acc += red_chain[w][r][s][gg][k];
-              code /= D;
-            }
-          }
         }
       }
+      // chain terms whose letter is z, in the fixed list order
+      const T* rc = &red_chain[0][0][s][0][0];
+      const int key = pc * D + z;
+#pragma unroll 1
+      for (int e = key_off[key]; e < key_off[key + 1]; ++e) acc += rc[key_idx[e]];
       partial[(((b - b0) * C::CPP + f.cip) * M + j0 + s) * D + z] = acc;
     }
     __syncthreads();

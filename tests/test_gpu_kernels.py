@@ -192,3 +192,52 @@ def test_full_size_properties(name):
         assert ora.rel_err(S[b:b + 1].detach().cpu().numpy(), ref) <= TOL32
         _, dref = ora.backward(x, ws.codes, ws.lengths, d, g[b:b + 1].double().cpu().numpy())
         assert ora.rel_err(dX[b:b + 1].cpu().numpy(), dref) <= TOL32
+
+
+@pytest.mark.parametrize("name", ["c1", "c3", "c4", "c5"])
+def test_windows_every_family(policy, name):
+    """signature_windows (reference sigcore.py:242-263) on each kernel family: (path, window)
+    pairs run as virtual paths; windows of different lengths share a CTA."""
+    ws = build_wordset(name, sk)
+    d = ws.d
+    X = brownian(7, 3, 40, d)
+    pairs = np.array([[0, 39], [5, 6], [10, 30], [0, 1], [38, 39], [3, 20], [1, 39]])
+    outs = sk.signature_windows(X, ws, sk.WindowSpec(pairs))
+    ref = ora.windows(X, ws.codes, ws.lengths, d, pairs)
+    assert len(outs) == len(pairs)
+    for k, o in enumerate(outs):
+        assert ora.rel_err(o.values, ref[:, k]) <= TOL64, k
+    # a whole-path window equals the forward signature bit for bit
+    assert np.array_equal(outs[0].values, sk.signature_forward(X, ws).values)
+    X32 = torch.from_numpy(X.astype(np.float32)).cuda()
+    outs32 = sk.signature_windows(X32, ws, sk.WindowSpec(pairs))
+    for k, o in enumerate(outs32):
+        assert ora.rel_err(o.cpu().numpy() if isinstance(o, torch.Tensor) else o.values.cpu().numpy(),
+                           ref[:, k]) <= TOL32, k
+
+
+@pytest.mark.parametrize("name", ["c4", "c5"])
+def test_backward_memory_contract(name):
+    """Memory-lean backward (reference test_acceptance.py:293-308): beyond its inputs, its
+    outputs and the per-step gradient partials (B x parts x M x d, the size class of dX),
+    the backward allocates nothing that grows with M -- no per-step signature trajectory."""
+    ws = build_wordset(name, sk)
+    d = ws.d
+    plan = ws.plan()
+    extra = []
+    for L in (101, 4001):
+        X = torch.from_numpy(brownian(1, 4, L, d).astype(np.float32)).cuda()
+        S = torch.empty((4, len(ws)), device="cuda")
+        plan.forward(X, S, 0, False)
+        g = torch.randn(4, len(ws), device="cuda")
+        dX = torch.empty_like(X)
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats()
+        base = torch.cuda.memory_allocated()
+        plan.backward(X, S, 0, False, g, 0, 0, dX)
+        torch.cuda.synchronize()
+        peak = torch.cuda.max_memory_allocated() - base
+        work = plan.workspace_bytes(torch.float32, 4, L, 0)
+        assert work <= 64 * 4 * (L - 1) * d * 4  # partials: at most 64 parts x dX
+        extra.append(peak - work)
+    assert extra[1] <= extra[0] + (1 << 20), extra  # independent of M (1 MiB slack for the allocator)
