@@ -388,11 +388,11 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
   T* Dl = Xs + C::PPC * (kChunkT + 1) * D;
   // per-warp per-step reduced gradients: leaf/mid letters, and chain terms per gp group
   T(*red_leaf)[RG::RGW][kChunkT][D] = reinterpret_cast<T(*)[RG::RGW][kChunkT][D]>(Dl + C::PPC * kChunkT * D);
-  T(*red_chain)[RG::RGW][kChunkT][RG::GPW][NCc] =
-      reinterpret_cast<T(*)[RG::RGW][kChunkT][RG::GPW][NCc]>(Dl + C::PPC * kChunkT * D + C::NW * RG::RGW * kChunkT * D);
+  T(*red_chain)[RG::RGW][kChunkT][RG::GPW][NCc] = reinterpret_cast<T(*)[RG::RGW][kChunkT][RG::GPW][NCc]>(
+      Dl + C::PPC * kChunkT * D + C::NW * RG::RGW * kChunkT * D);
   // per-(path slot, letter) lists of this CTA's parked chain terms, built once:
   // replaces a per-element scan of every chain term in the chunk epilogue
-  int* key_off = reinterpret_cast<int*>(reinterpret_cast<T*>(Dl + C::PPC * kChunkT * D + C::NW * RG::RGW * kChunkT * D) +
+  int* key_off = reinterpret_cast<int*>(Dl + C::PPC * kChunkT * D + C::NW * RG::RGW * kChunkT * D +
                                         C::NW * RG::RGW * kChunkT * RG::GPW * NCc);
   unsigned short* key_idx = reinterpret_cast<unsigned short*>(key_off + RG::NKEY + 1);
   const int64_t cta = blockIdx.x + (C::CPP > 1 ? b0 * C::CPP : b0 / C::PPC);
@@ -494,7 +494,8 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
         gm[g] = fma(lm, tN1, tb * tN * inv<T, 2>());
         lam.mid[g] = lm + tb;
       }
-      // mids' gradient terms join the leaf letters
+      // mids' gradient terms join the leaf letters (letter q*G + g).  A separate
+      // butterfly over the grand-parent lanes was measured slower (more SHFL).
       if constexpr (G == D) {
 #pragma unroll
         for (int g = 0; g < G; ++g) gl[g] += gm[g];
