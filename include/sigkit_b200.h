@@ -53,7 +53,8 @@ const char* sigb_last_error(void);
 int sigb_device_sm_count(void);
 /* Kernel routing: 0 = auto (register-resident truncated kernels where an
  * instantiation exists, else fragment kernels, else level kernels),
- * 1 = level kernels only, 2 = fragment kernels (then level kernels).
+ * 1 = level kernels only, 2 = fragment kernels (then level kernels),
+ * 3 = level-slot kernels for small sparse tries (then level kernels).
  * Process-wide; used by the tests to check both paths against the oracle. */
 int sigb_set_kernel_policy(int policy);
 /* Number of device kernels this library has launched (process-wide). */
@@ -106,7 +107,8 @@ int64_t sigb_plan_num_parts(const sigb_plan* plan);
 int64_t sigb_plan_step_fmas(const sigb_plan* plan);
 /* Kernel family sigb_forward / sigb_backward will run for this plan under the
  * current policy: 1 = register-resident truncated kernels, 2 = register-resident
- * fragment kernels (any trie), 0 = level-synchronous trie kernels, -1 = NULL plan. */
+ * fragment kernels (any trie), 3 = level-slot kernels (small tries, one CTA per
+ * path), 0 = level-synchronous trie kernels, -1 = NULL plan. */
 int sigb_plan_kernel_kind(const sigb_plan* plan);
 /* Host-only (no device): the fragment decomposition the plan would use for
  * this word set.  info[8] = {NC, G, K, fragments, CTAs per path, |cl(I)|,

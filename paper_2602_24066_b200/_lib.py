@@ -86,7 +86,7 @@ def check(rc: int) -> None:
 
 
 def set_kernel_policy(policy: int) -> None:
-    """0 = auto (truncated > fragment > level kernels), 1 = level kernels only, 2 = fragment kernels first."""
+    """0 auto (truncated > slot | fragment > level), 1 level only, 2 fragment first, 3 level-slot first."""
     check(lib().sigb_set_kernel_policy(int(policy)))
 
 

@@ -160,8 +160,17 @@ int backward_t(const sigb_plan* p, const void* X, int64_t B, int64_t L, const vo
 }
 
 bool use_trunc(const sigb_plan* p) { return g_policy == 0 && p->trunc_depth >= 2 && trunc::supported(p->d, p->trunc_depth); }
-// policy 0: truncated > fragment > level; 1: level only; 2: fragment > level
-bool use_frag(const sigb_plan* p) { return g_policy != 1 && p->frag.ok && !use_trunc(p); }
+// policy 0: truncated > (slot | fragment, the planner's choice) > level; 1: level only;
+// 2: fragment > level; 3: slot > level
+bool use_slot(const sigb_plan* p) {
+  if (!p->slot.ok) return false;
+  if (g_policy == 3) return true;
+  return g_policy == 0 && !use_trunc(p) && p->prefer_slot;
+}
+bool use_frag(const sigb_plan* p) {
+  if (!p->frag.ok || g_policy == 1 || g_policy == 3) return false;
+  return g_policy == 2 || (!use_trunc(p) && !use_slot(p));
+}
 
 int check_common(const sigb_plan* p, int dtype, int64_t B, int64_t L) {
   if (!p) return fail(SIGB_ERR_DOMAIN, "plan is NULL");
@@ -178,11 +187,12 @@ using namespace sigb;
 
 extern "C" int sigb_version(void) { return 100; }
 extern "C" int sigb_plan_kernel_kind(const sigb_plan* plan) {
-  return plan ? (use_trunc(plan) ? 1 : use_frag(plan) ? 2 : 0) : -1;
+  return plan ? (use_trunc(plan) ? 1 : use_slot(plan) ? 3 : use_frag(plan) ? 2 : 0) : -1;
 }
 extern "C" int sigb_set_kernel_policy(int policy) {
-  if (policy < 0 || policy > 2)
-    return fail(SIGB_ERR_DOMAIN, "kernel policy must be 0 (auto), 1 (level kernels) or 2 (fragment kernels)");
+  if (policy < 0 || policy > 3)
+    return fail(SIGB_ERR_DOMAIN,
+                "kernel policy must be 0 (auto), 1 (level kernels), 2 (fragment kernels) or 3 (level-slot kernels)");
   g_policy = policy;
   return SIGB_OK;
 }
@@ -234,6 +244,8 @@ extern "C" int sigb_forward(const sigb_plan* plan, int dtype, const void* d_X, i
     return trunc::forward(dtype, plan->d, plan->trunc_depth, d_X, B, L, nullptr, 1, d_out, out_ld, out_col0, include_empty,
                           (cudaStream_t)stream);
   }
+  if (use_slot(plan))
+    return slot::forward(plan, dtype, d_X, B, L, d_out, out_ld, out_col0, include_empty, d_state, (cudaStream_t)stream);
   if (use_frag(plan))
     return frag::forward(plan, dtype, d_X, B, L, nullptr, 1, d_out, out_ld, out_col0, include_empty, d_state,
                          (cudaStream_t)stream);
@@ -253,7 +265,7 @@ extern "C" int sigb_windows(const sigb_plan* plan, int dtype, const void* d_X, i
   if (use_trunc(plan))
     return trunc::forward(dtype, plan->d, plan->trunc_depth, d_X, B * K, L, d_bounds, K, d_out, plan->W, 0, 0,
                           (cudaStream_t)stream);
-  if (use_frag(plan))
+  if (plan->frag.ok && (g_policy == 0 || g_policy == 2) && !use_trunc(plan))  // slot kernels have no windowed form
     return frag::forward(plan, dtype, d_X, B * K, L, d_bounds, K, d_out, plan->W, 0, 0, nullptr, (cudaStream_t)stream);
   if (dtype == SIGB_F32)
     return forward_t<float>(plan, d_X, B, L, d_bounds, K, d_out, plan->W, 0, 0, nullptr, nullptr, 0, 0,
@@ -270,6 +282,10 @@ extern "C" int sigb_backward_workspace_size(const sigb_plan* plan, int dtype, in
   if (B == 0 || L == 1) { *bytes = 0; return SIGB_OK; }
   if (use_trunc(plan) && ckpt_stride == 0) {
     *bytes = trunc::backward_workspace(dtype, plan->d, plan->trunc_depth, B, L);
+    return SIGB_OK;
+  }
+  if (use_slot(plan) && ckpt_stride == 0) {
+    *bytes = slot::backward_workspace(plan, dtype, B, L);
     return SIGB_OK;
   }
   if (use_frag(plan) && ckpt_stride == 0) {
@@ -299,6 +315,11 @@ extern "C" int sigb_backward(const sigb_plan* plan, int dtype, const void* d_X, 
     if (s_is_state) { s_ld = plan->Wc; s_col0 = 0; }
     return trunc::backward(dtype, plan->d, plan->trunc_depth, d_X, B, L, d_S, s_ld, s_col0, d_g, g_ld, g_col0, d_work,
                            work_bytes, d_dX, d_dinc, (cudaStream_t)stream);
+  }
+  if (use_slot(plan) && ckpt_stride == 0 && B > 0 && L > 1) {
+    if (s_is_state) { s_ld = plan->Wc; s_col0 = 0; }
+    return slot::backward(plan, dtype, d_X, B, L, d_S, s_ld, s_col0, d_g, g_ld, g_col0, d_work, work_bytes, d_dX,
+                          d_dinc, (cudaStream_t)stream);
   }
   if (use_frag(plan) && ckpt_stride == 0 && B > 0 && L > 1) {
     if (s_is_state) { s_ld = plan->Wc; s_col0 = 0; }

@@ -369,13 +369,17 @@ __global__ void __launch_bounds__(kTPB) frag_backward_kernel(FragDev fd, const T
       // (d) park this step's gradient terms at their letter-major offsets
       T* pb = buf + (size_t)nbuf * fd.pstride;
 #pragma unroll
-      for (int k = 0; k < NC; ++k) pb[pos[k]] = gch[k];
+      for (int k = 0; k < NC; ++k)
+        if (pos[k] != 0xFFFF) pb[pos[k]] = gch[k];
 #pragma unroll
-      for (int g = 0; g < G; ++g) pb[pos[NC + g]] = gm[g];
+      for (int g = 0; g < G; ++g)
+        if (pos[NC + g] != 0xFFFF) pb[pos[NC + g]] = gm[g];
 #pragma unroll
-      for (int k = 0; k < K; ++k) pb[pos[NC + G + k]] = gl[k];
+      for (int k = 0; k < K; ++k)
+        if (pos[NC + G + k] != 0xFFFF) pb[pos[NC + G + k]] = gl[k];
 #pragma unroll
-      for (int k = 0; k < K; ++k) pb[pos[NC + G + K + k]] = ga[k];
+      for (int k = 0; k < K; ++k)
+        if (pos[NC + G + K + k] != 0xFFFF) pb[pos[NC + G + K + k]] = ga[k];
       ++nbuf;
       if (nbuf == kRedSteps || s == 0) {
         __syncthreads();

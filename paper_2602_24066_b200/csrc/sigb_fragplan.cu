@@ -232,7 +232,7 @@ bool plan_fragments(const Trie& t, FragHost& out, std::string& why) {
     }
   // per CTA-part letter-major parking layout for the backward's gradient terms:
   // letter z's entries are contiguous (slot-major, then thread), each letter
-  // block padded to a float4; slots without a letter write to a trash float.
+  // block padded to a float4; slots without a letter (0xFFFF) are not parked.
   out.pos.assign((size_t)NGS * Fp, 0);
   out.red_off.assign((size_t)cpp * (t.d + 1), 0);
   int pmax = 0;
@@ -246,17 +246,16 @@ bool plan_fragments(const Trie& t, FragHost& out, std::string& why) {
     std::vector<int> base(t.d + 1, 0);
     for (int z = 0; z < t.d; ++z) base[z + 1] = base[z] + (cnt[z] + 3) / 4 * 4;
     for (int z = 0; z <= t.d; ++z) out.red_off[(size_t)c * (t.d + 1) + z] = base[z] / 4;
-    const int trash = base[t.d];
     std::vector<int> fill(base.begin(), base.end() - 1);
     for (int slot = 0; slot < NGS; ++slot)
       for (int tid = 0; tid < TPB; ++tid) {
         const size_t i = (size_t)slot * Fp + c * TPB + tid;
         const int z = out.letter[i];
-        out.pos[i] = (unsigned short)(z < t.d ? fill[z]++ : trash);
+        out.pos[i] = (unsigned short)(z < t.d ? fill[z]++ : 0xFFFF);  // no letter: not parked
       }
-    pmax = std::max(pmax, trash + 4);
+    pmax = std::max(pmax, base[t.d]);
   }
-  if (pmax > 65535) {
+  if (pmax >= 65535) {
     why = "fragment gradient buffer exceeds 16-bit offsets";
     return false;
   }

@@ -87,6 +87,26 @@ struct FragHost {
 // shape; false (with `why`) when no instantiation fits.
 bool plan_fragments(const Trie& t, FragHost& out, std::string& why);
 
+// Host image of a level-slot plan (sigb_slot.cuh).  Slot arrays are [KS][TPB].
+struct SlotHost {
+  int N = 0, TPB = 0;
+  int a_off = 0, t_off = 0, t_size = 0, park_off = 0, tm_off = 0, p_off = 0, p_size = 0, pstride = 0;
+  int fwd_smem = 0, bwd_smem = 0;  // elements
+  std::vector<int> tinfo, lvl, red_off, cidx, eidx;
+  std::vector<unsigned> meta0, meta1;
+  std::vector<unsigned short> pos;
+};
+bool plan_slots(const Trie& t, SlotHost& out, std::string& why);
+
+struct SlotDevPlan {
+  bool ok = false;
+  SlotHost h;  // scalars (device copies below)
+  int* tinfo = nullptr;
+  unsigned *meta0 = nullptr, *meta1 = nullptr;
+  unsigned short* pos = nullptr;
+  int *cidx = nullptr, *eidx = nullptr, *lvl = nullptr, *red_off = nullptr;
+};
+
 struct FragDevPlan {
   bool ok = false;
   int NC = 0, G = 0, K = 0, F = 0, cpp = 0, Fp = 0, pstride = 0;
@@ -117,6 +137,8 @@ struct sigb_plan {
   int* d_lseg = nullptr;
   std::vector<sigb::PartDesc> h_parts;
   sigb::FragDevPlan frag;  // register-resident fragment kernels (sigb_frag.cuh), when ok
+  sigb::SlotDevPlan slot;  // level-slot kernels for small sparse tries (sigb_slot.cuh), when ok
+  bool prefer_slot = false;  // the planner's choice between slot and fragment kernels
 
   sigb::PlanDev dev() const {
     sigb::PlanDev p;
@@ -150,6 +172,15 @@ int backward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L,
              int64_t s_col0, const void* g, int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, void* dX,
              void* dinc, cudaStream_t stream);
 }  // namespace frag
+namespace slot {
+bool supported(int N);
+int forward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, void* out, int64_t out_ld,
+            int64_t out_col0, int include_empty, void* state, cudaStream_t stream);
+size_t backward_workspace(const sigb_plan* p, int dtype, int64_t B, int64_t L);
+int backward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, const void* S, int64_t s_ld,
+             int64_t s_col0, const void* g, int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, void* dX,
+             void* dinc, cudaStream_t stream);
+}  // namespace slot
 namespace trunc {
 bool supported(int64_t d, int depth);
 int forward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L, const int64_t* bounds, int64_t K,

@@ -320,6 +320,34 @@ extern "C" int sigb_plan_create(const uint64_t* codes, const int64_t* lengths, i
       fp.ok = true;
     }
   }
+  // level-slot plan (sigb_slot.cuh) for small sparse tries
+  {
+    SlotHost sh;
+    std::string why;
+    if (plan_slots(t, sh, why) && slot::supported(sh.N)) {
+      SlotDevPlan& sp = plan->slot;
+      int rc3;
+      auto up = [&](auto** dst, const auto& src) -> int {
+        using E = typename std::remove_reference<decltype(src)>::type::value_type;
+        SIGB_CUDA_TRY(cudaMalloc((void**)dst, sizeof(E) * std::max<size_t>(src.size(), 1)));
+        if (!src.empty())
+          SIGB_CUDA_TRY(cudaMemcpyAsync((void*)*dst, src.data(), sizeof(E) * src.size(), cudaMemcpyHostToDevice, stream));
+        return SIGB_OK;
+      };
+      if ((rc3 = up(&sp.tinfo, sh.tinfo)) || (rc3 = up(&sp.meta0, sh.meta0)) || (rc3 = up(&sp.meta1, sh.meta1)) ||
+          (rc3 = up(&sp.pos, sh.pos)) || (rc3 = up(&sp.cidx, sh.cidx)) || (rc3 = up(&sp.eidx, sh.eidx)) ||
+          (rc3 = up(&sp.lvl, sh.lvl)) || (rc3 = up(&sp.red_off, sh.red_off))) {
+        sigb_plan_destroy(plan);
+        return rc3;
+      }
+      sp.h = sh;
+      sp.h.tinfo.clear(); sp.h.meta0.clear(); sp.h.meta1.clear(); sp.h.pos.clear();
+      sp.h.cidx.clear(); sp.h.eidx.clear();
+      sp.ok = true;
+      // sparse tries (few words per fragment) run faster with one node per slot
+      plan->prefer_slot = !plan->frag.ok || (double)Wc / std::max(plan->frag.F, 1) < 12.0;
+    }
+  }
   // perm is stored per part at node_off (same offsets as the node tables)
   auto upload = [&](auto** dst, const auto& src) -> int {
     using E = typename std::remove_reference<decltype(src)>::type::value_type;
@@ -355,6 +383,8 @@ extern "C" int sigb_plan_destroy(sigb_plan* plan) {
   cudaFree(plan->frag.sidx);
   cudaFree(plan->frag.pos);
   cudaFree(plan->frag.red_off);
+  cudaFree(plan->slot.tinfo); cudaFree(plan->slot.meta0); cudaFree(plan->slot.meta1); cudaFree(plan->slot.pos);
+  cudaFree(plan->slot.cidx); cudaFree(plan->slot.eidx); cudaFree(plan->slot.lvl); cudaFree(plan->slot.red_off);
   delete plan;
   return SIGB_OK;
 }
