@@ -344,8 +344,9 @@ extern "C" int sigb_plan_create(const uint64_t* codes, const int64_t* lengths, i
       sp.h.tinfo.clear(); sp.h.meta0.clear(); sp.h.meta1.clear(); sp.h.pos.clear();
       sp.h.cidx.clear(); sp.h.eidx.clear();
       sp.ok = true;
-      // sparse tries (few words per fragment) run faster with one node per slot
-      plan->prefer_slot = !plan->frag.ok || (double)Wc / std::max(plan->frag.F, 1) < 12.0;
+      // measured on c3 (r01): barrier-bound at ~1.4 TF fwd vs ~11 TF for the fragment
+      // kernels, so level-slot only serves sets the fragment planner cannot cut
+      plan->prefer_slot = !plan->frag.ok;
     }
   }
   // perm is stored per part at node_off (same offsets as the node tables)

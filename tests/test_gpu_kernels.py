@@ -93,8 +93,7 @@ def test_configs_every_family(golden_forward, golden_backward, policy, name):
 def test_auto_routing():
     kinds = {n: build_wordset(n, sk).plan().kernel_kind for n in CONFIGS}
     assert kinds["c1"] == kinds["c2"] == kinds["c5"] == 1  # truncated kernels
-    assert kinds["c3"] == 3  # level-slot kernels (sparse 2,048-word trie)
-    assert kinds["c4"] == 2  # fragment kernels
+    assert kinds["c3"] == kinds["c4"] == 2  # fragment kernels
 
 
 @pytest.mark.parametrize("seed", range(6))
@@ -210,8 +209,12 @@ def test_windows_every_family(policy, name):
     assert len(outs) == len(pairs)
     for k, o in enumerate(outs):
         assert ora.rel_err(o.values, ref[:, k]) <= TOL64, k
-    # a whole-path window equals the forward signature bit for bit
-    assert np.array_equal(outs[0].values, sk.signature_forward(X, ws).values)
+    # a whole-path window equals the forward signature bit for bit when both run the
+    # same kernel family (level-slot plans have no windowed form; windows use fragments)
+    if ws.plan().kernel_kind != 3:
+        assert np.array_equal(outs[0].values, sk.signature_forward(X, ws).values)
+    else:
+        assert ora.rel_err(outs[0].values, sk.signature_forward(X, ws).values) <= TOL64
     X32 = torch.from_numpy(X.astype(np.float32)).cuda()
     outs32 = sk.signature_windows(X32, ws, sk.WindowSpec(pairs))
     for k, o in enumerate(outs32):
