@@ -105,7 +105,8 @@ __device__ __forceinline__ void chain_partials(const FState<T, NC, G, K>& st, co
   }
 }
 
-template <typename T, int NC, int G, int K>
+// Leaves = false (backward reconstruction): leaf values are never read there.
+template <typename T, int NC, int G, int K, bool Leaves = true>
 __device__ __forceinline__ void chen_step(FState<T, NC, G, K>& st, const FIncr<T, NC, G, K>& in) {
   constexpr int NV = NC + 2;
   T tch[NC][NC + 3];
@@ -116,13 +117,17 @@ __device__ __forceinline__ void chen_step(FState<T, NC, G, K>& st, const FIncr<T
   for (int k = 0; k < NC; ++k) st.ch[k] = tch[k][k + 1];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    const T tm = fma(in.dy[g] * T(0.5), tN, st.mid[g]);  // T(mid_g, NV)
+    if constexpr (Leaves) {
+      const T tm = fma(in.dy[g] * T(0.5), tN, st.mid[g]);  // T(mid_g, NV)
+#pragma unroll
+      for (int k = 0; k < K; ++k) st.leaf[g][k] = fma(in.dz[k], tm, st.leaf[g][k]);
+    }
     st.mid[g] = fma(in.dy[g], tN1, st.mid[g]);
-#pragma unroll
-    for (int k = 0; k < K; ++k) st.leaf[g][k] = fma(in.dz[k], tm, st.leaf[g][k]);
   }
+  if constexpr (Leaves) {
 #pragma unroll
-  for (int k = 0; k < K; ++k) st.al[k] = fma(in.da[k], tN1, st.al[k]);
+    for (int k = 0; k < K; ++k) st.al[k] = fma(in.da[k], tN1, st.al[k]);
+  }
 }
 
 // Device view of a fragment plan.  Per-fragment arrays are slot-major
@@ -302,9 +307,9 @@ __global__ void __launch_bounds__(kTPB) frag_backward_kernel(FragDev fd, const T
     for (int s = cs - 1; s >= 0; --s) {
       const T* row = Dl + s * (d + 1);
       FIncr<T, NC, G, K> in;
-      // (a) S_{0,t_{j+1}} -> S_{0,t_j}
+      // (a) S_{0,t_{j+1}} -> S_{0,t_j} (chain and mids; leaf values are never read)
       gather<T, NC, G, K>(row, lt, T(-1), in);
-      chen_step<T, NC, G, K>(st, in);
+      chen_step<T, NC, G, K, false>(st, in);
       // (b) forward partials from S_{0,t_j}
       gather<T, NC, G, K>(row, lt, T(1), in);
       T tch[NC][NC + 3];

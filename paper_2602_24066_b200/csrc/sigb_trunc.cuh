@@ -243,7 +243,10 @@ __device__ __forceinline__ void chain_partials(const State<T, D, N, G>& st, cons
 }
 
 // One forward Chen step S <- S ⊗ exp(dX) on the fragment (in.* already signed).
-template <typename T, int D, int N, int G>
+// Leaves = false skips the leaf values: the backward never reads a leaf's S
+// (a leaf's adjoint is constant in time and its gradient term uses its
+// parent's partial), so its reconstruction would be pure waste (G*D FMAs/step).
+template <typename T, int D, int N, int G, bool Leaves = true>
 __device__ __forceinline__ void chen_step(State<T, D, N, G>& st, const StepIncr<T, D, N, G>& in) {
   constexpr int NC = Cfg<D, N, G>::NC;
   T tch[NC > 0 ? NC : 1][N + 1];
@@ -254,10 +257,12 @@ __device__ __forceinline__ void chen_step(State<T, D, N, G>& st, const StepIncr<
   for (int k = 0; k < NC; ++k) st.ch[k] = tch[k][k + 1];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    const T tm = fma(in.dy[g] * inv<T, 2>(), tN, st.mid[g]);  // T(u_g, N)
-    st.mid[g] = fma(in.dy[g], tN1, st.mid[g]);
+    if constexpr (Leaves) {
+      const T tm = fma(in.dy[g] * inv<T, 2>(), tN, st.mid[g]);  // T(u_g, N)
 #pragma unroll
-    for (int z = 0; z < D; ++z) st.leaf[g][z] = fma(in.dz[z], tm, st.leaf[g][z]);
+      for (int z = 0; z < D; ++z) st.leaf[g][z] = fma(in.dz[z], tm, st.leaf[g][z]);
+    }
+    st.mid[g] = fma(in.dy[g], tN1, st.mid[g]);
   }
 }
 
@@ -418,7 +423,7 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
       lam.mid[g] = live ? grow[f.mid_index(g)] : T(0);
 #pragma unroll
       for (int z = 0; z < D; ++z) {
-        st.leaf[g][z] = live ? srow[f.leaf_index(g, z)] : T(0);
+        st.leaf[g][z] = T(0);  // never read by the backward
         lam.leaf[g][z] = live ? grow[f.leaf_index(g, z)] : T(0);
       }
     }
@@ -454,9 +459,9 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
 #pragma unroll 1
     for (int s = cs - 1; s >= 0; --s) {
       StepIncr<T, D, N, G> in;
-      // (a) rebuild S_{0,t_j} = S_{0,t_{j+1}} ⊗ exp(-dX_j)
+      // (a) rebuild S_{0,t_j} = S_{0,t_{j+1}} ⊗ exp(-dX_j) (chain and mids only)
       in.load(rows + s * D, f, T(-1));
-      chen_step<T, D, N, G>(st, in);
+      chen_step<T, D, N, G, false>(st, in);
       // (b) forward partials from S_{0,t_j}
 #pragma unroll
       for (int i = 0; i < D; ++i) in.dz[i] = -in.dz[i];
