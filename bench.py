@@ -391,6 +391,8 @@ def run_ours(args) -> None:
     bytes_bwd = (2 * L * d + 2 * W) * s_el
     prefix = {1: "trunc_", 2: "frag_", 3: "slot_"}.get(plan.kernel_kind, "")
     kb_name, kf_name = prefix + "backward_kernel", prefix + "forward_kernel"
+    if plan.kernel_kind == 4:
+        kb_name, kf_name = "sigjit_bwd", "sigjit_fwd"
     roof_b = roof(kb_name, f_bwd_path, kb_ms, kb_n, bytes_bwd)
     roof_f = roof(kf_name, f_fwd_path, kf_ms, kf_n, bytes_fwd)
     dominant = roof_b if (roof_b and kb_ms >= kf_ms) else roof_f
@@ -526,7 +528,7 @@ def run_ours(args) -> None:
                        "l2": "no flush: every pass streams inputs larger than L2 (X %.2f GB, S %.2f GB per rank)"
                              % (B * L * d * s_el / 1e9, B * W * s_el / 1e9),
                        "kernels": {1: "truncated register-resident", 2: "fragment register-resident",
-                                   3: "level-slot"}.get(
+                                   3: "level-slot", 4: "word-set generated (NVRTC)"}.get(
                            plan.kernel_kind, "level-synchronous trie")},
             "fwd": {"value": fwd_value, "unit": "paths/s", "ms_per_step": fwd_ms / args.steps},
             "roofline": dominant, "roofline_fwd": roof_f if dominant is not roof_f else roof_b,

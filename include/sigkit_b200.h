@@ -54,7 +54,8 @@ int sigb_device_sm_count(void);
 /* Kernel routing: 0 = auto (register-resident truncated kernels where an
  * instantiation exists, else fragment kernels, else level kernels),
  * 1 = level kernels only, 2 = fragment kernels (then level kernels),
- * 3 = level-slot kernels for small sparse tries (then level kernels).
+ * 3 = level-slot kernels for small sparse tries (then level kernels),
+ * 4 = word-set-specialised generated kernels (then fragment, level kernels).
  * Process-wide; used by the tests to check both paths against the oracle. */
 int sigb_set_kernel_policy(int policy);
 /* Number of device kernels this library has launched (process-wide). */
@@ -108,13 +109,20 @@ int64_t sigb_plan_step_fmas(const sigb_plan* plan);
 /* Kernel family sigb_forward / sigb_backward will run for this plan under the
  * current policy: 1 = register-resident truncated kernels, 2 = register-resident
  * fragment kernels (any trie), 3 = level-slot kernels (small tries, one CTA per
- * path), 0 = level-synchronous trie kernels, -1 = NULL plan. */
+ * path), 4 = word-set-specialised generated kernels (small sparse sets),
+ * 0 = level-synchronous trie kernels, -1 = NULL plan. */
 int sigb_plan_kernel_kind(const sigb_plan* plan);
 /* Host-only (no device): the fragment decomposition the plan would use for
  * this word set.  info[8] = {NC, G, K, fragments, CTAs per path, |cl(I)|,
  * estimated issue slots per path-step, instantiated (0/1)}.  Fails with
  * SIGB_ERR_UNSUPPORTED when no fragment shape fits. */
 int sigb_fragment_plan_info(const uint64_t* codes, const int64_t* lengths, int64_t W, int64_t d, int64_t* info);
+/* Host-only: the CUDA source generated for a small word set (the plan
+ * compiles it with NVRTC for sm_100a on first use; policy 4 / auto for sparse
+ * sets).  Writes at most cap-1 bytes + NUL to buf (may be NULL) and the full
+ * length to *len.  SIGB_ERR_UNSUPPORTED when the set is too large. */
+int sigb_jit_source(const uint64_t* codes, const int64_t* lengths, int64_t W, int64_t d, int dtype, int backward,
+                    char* buf, size_t cap, size_t* len);
 
 /*
  * Forward signature.  Replaces forward_kernel (_kernels.py:40-58) together

@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsigkit_b200.so")
-SOURCES = ["sigb_api.cu", "sigb_plan.cu", "sigb_tables.cu", "sigb_trunc.cu", "sigb_frag.cu", "sigb_fragplan.cu", "sigb_slot.cu", "sigb_slotplan.cu"]
+SOURCES = ["sigb_api.cu", "sigb_plan.cu", "sigb_tables.cu", "sigb_trunc.cu", "sigb_frag.cu", "sigb_fragplan.cu", "sigb_slot.cu", "sigb_slotplan.cu", "sigb_jit.cu"]
 DEPS = SOURCES + ["sigb_internal.h", "sigb_level.cu", "sigb_trunc.cuh", "sigb_frag.cuh", "sigb_slot.cuh"]
 
 NVCC_FLAGS = [
@@ -20,6 +20,8 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
     "-Xptxas", "-v",
+    # NVRTC compiles the word-set-specialised kernels at run time (sigb_jit.cu)
+    "-lnvrtc", "-Xlinker", "-rpath,/usr/local/cuda/lib64",
 ]
 
 

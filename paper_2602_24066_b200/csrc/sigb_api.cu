@@ -159,17 +159,25 @@ int backward_t(const sigb_plan* p, const void* X, int64_t B, int64_t L, const vo
   return SIGB_OK;
 }
 
+
+// policy 0: truncated > generated (small sparse sets) > (slot | fragment) > level; 1: level only;
+// 2: fragment > level; 3: slot > level; 4: generated > fragment > level
 bool use_trunc(const sigb_plan* p) { return g_policy == 0 && p->trunc_depth >= 2 && trunc::supported(p->d, p->trunc_depth); }
-// policy 0: truncated > (slot | fragment, the planner's choice) > level; 1: level only;
-// 2: fragment > level; 3: slot > level
+bool use_jit(const sigb_plan* p) {
+  if (!p->jit.eligible || p->jit.broken || g_policy == 1 || g_policy == 2 || g_policy == 3) return false;
+  if (g_policy == 4) return true;
+  if (use_trunc(p)) return false;
+  // sparse sets: few words per fragment (the fragment kernels replicate chains there)
+  return !p->frag.ok || (double)p->Wc / std::max(p->frag.F, 1) < 12.0;
+}
 bool use_slot(const sigb_plan* p) {
   if (!p->slot.ok) return false;
   if (g_policy == 3) return true;
-  return g_policy == 0 && !use_trunc(p) && p->prefer_slot;
+  return g_policy == 0 && !use_trunc(p) && !use_jit(p) && p->prefer_slot;
 }
 bool use_frag(const sigb_plan* p) {
   if (!p->frag.ok || g_policy == 1 || g_policy == 3) return false;
-  return g_policy == 2 || (!use_trunc(p) && !use_slot(p));
+  return g_policy == 2 || (!use_trunc(p) && !use_slot(p) && !use_jit(p));
 }
 
 int check_common(const sigb_plan* p, int dtype, int64_t B, int64_t L) {
@@ -187,12 +195,12 @@ using namespace sigb;
 
 extern "C" int sigb_version(void) { return 100; }
 extern "C" int sigb_plan_kernel_kind(const sigb_plan* plan) {
-  return plan ? (use_trunc(plan) ? 1 : use_slot(plan) ? 3 : use_frag(plan) ? 2 : 0) : -1;
+  return plan ? (use_trunc(plan) ? 1 : use_jit(plan) ? 4 : use_slot(plan) ? 3 : use_frag(plan) ? 2 : 0) : -1;
 }
 extern "C" int sigb_set_kernel_policy(int policy) {
-  if (policy < 0 || policy > 3)
-    return fail(SIGB_ERR_DOMAIN,
-                "kernel policy must be 0 (auto), 1 (level kernels), 2 (fragment kernels) or 3 (level-slot kernels)");
+  if (policy < 0 || policy > 4)
+    return fail(SIGB_ERR_DOMAIN, "kernel policy must be 0 (auto), 1 (level kernels), 2 (fragment kernels), "
+                                 "3 (level-slot kernels) or 4 (generated kernels)");
   g_policy = policy;
   return SIGB_OK;
 }
@@ -244,6 +252,10 @@ extern "C" int sigb_forward(const sigb_plan* plan, int dtype, const void* d_X, i
     return trunc::forward(dtype, plan->d, plan->trunc_depth, d_X, B, L, nullptr, 1, d_out, out_ld, out_col0, include_empty,
                           (cudaStream_t)stream);
   }
+  if (use_jit(plan)) {
+    rc = jit::forward(plan, dtype, d_X, B, L, d_out, out_ld, out_col0, include_empty, d_state, (cudaStream_t)stream);
+    if (rc == SIGB_OK || g_policy == 4) return rc;  // else: compilation failed, fall back
+  }
   if (use_slot(plan))
     return slot::forward(plan, dtype, d_X, B, L, d_out, out_ld, out_col0, include_empty, d_state, (cudaStream_t)stream);
   if (use_frag(plan))
@@ -284,6 +296,10 @@ extern "C" int sigb_backward_workspace_size(const sigb_plan* plan, int dtype, in
     *bytes = trunc::backward_workspace(dtype, plan->d, plan->trunc_depth, B, L);
     return SIGB_OK;
   }
+  if (use_jit(plan) && ckpt_stride == 0 && jit::ensure(const_cast<sigb_plan*>(plan), dtype, true) == SIGB_OK) {
+    *bytes = jit::backward_workspace(plan, dtype, B, L);
+    return SIGB_OK;
+  }
   if (use_slot(plan) && ckpt_stride == 0) {
     *bytes = slot::backward_workspace(plan, dtype, B, L);
     return SIGB_OK;
@@ -315,6 +331,12 @@ extern "C" int sigb_backward(const sigb_plan* plan, int dtype, const void* d_X, 
     if (s_is_state) { s_ld = plan->Wc; s_col0 = 0; }
     return trunc::backward(dtype, plan->d, plan->trunc_depth, d_X, B, L, d_S, s_ld, s_col0, d_g, g_ld, g_col0, d_work,
                            work_bytes, d_dX, d_dinc, (cudaStream_t)stream);
+  }
+  if (use_jit(plan) && ckpt_stride == 0 && B > 0 && L > 1 &&
+      jit::ensure(const_cast<sigb_plan*>(plan), dtype, true) == SIGB_OK) {
+    if (s_is_state) { s_ld = plan->Wc; s_col0 = 0; }
+    return jit::backward(plan, dtype, d_X, B, L, d_S, s_ld, s_col0, d_g, g_ld, g_col0, d_work, work_bytes, d_dX,
+                         d_dinc, (cudaStream_t)stream);
   }
   if (use_slot(plan) && ckpt_stride == 0 && B > 0 && L > 1) {
     if (s_is_state) { s_ld = plan->Wc; s_col0 = 0; }

@@ -107,6 +107,39 @@ struct SlotDevPlan {
   int *cidx = nullptr, *eidx = nullptr, *lvl = nullptr, *red_off = nullptr;
 };
 
+// Word-set-specialised (NVRTC) kernels for small tries (sigb_jit.cu).
+namespace jit {
+struct Task {
+  std::vector<int64_t> nodes;  // closure indices: chain (levels 1..c) then bodies, topological
+  int chain = 0;               // leading chain nodes (replicated; the first task containing one owns it)
+};
+}  // namespace jit
+struct JitHost {
+  std::vector<jit::Task> fwd_tasks, bwd_tasks;
+};
+struct JitPlan {
+  bool eligible = false;       // small enough for generated code
+  Trie trie;                   // closure (kept for lazy code generation)
+  JitHost host;
+  // compiled kernels per [dtype][backward]; failed = compile attempted and failed
+  void* lib[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  void* kern[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  bool failed[2][2] = {{false, false}, {false, false}};
+  bool broken = false;  // some compilation failed: route this plan elsewhere
+};
+namespace jit {
+bool eligible(const Trie& t);
+void make_plan(const Trie& t, JitHost& h);
+std::string source(const Trie& t, const JitHost& h, int dtype, bool backward);
+int ensure(sigb_plan* p, int dtype, bool backward);  // compile / load; SIGB_OK or error
+int forward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, void* out, int64_t out_ld,
+            int64_t out_col0, int include_empty, void* state, cudaStream_t stream);
+size_t backward_workspace(const sigb_plan* p, int dtype, int64_t B, int64_t L);
+int backward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, const void* S, int64_t s_ld,
+             int64_t s_col0, const void* g, int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, void* dX,
+             void* dinc, cudaStream_t stream);
+}  // namespace jit
+
 struct FragDevPlan {
   bool ok = false;
   int NC = 0, G = 0, K = 0, F = 0, cpp = 0, Fp = 0, pstride = 0;
@@ -138,6 +171,7 @@ struct sigb_plan {
   std::vector<sigb::PartDesc> h_parts;
   sigb::FragDevPlan frag;  // register-resident fragment kernels (sigb_frag.cuh), when ok
   sigb::SlotDevPlan slot;  // level-slot kernels for small sparse tries (sigb_slot.cuh), when ok
+  sigb::JitPlan jit;       // word-set-specialised kernels (sigb_jit.cu), when eligible
   bool prefer_slot = false;  // the planner's choice between slot and fragment kernels
 
   sigb::PlanDev dev() const {

@@ -163,6 +163,24 @@ extern "C" int sigb_fragment_plan_info(const uint64_t* codes, const int64_t* len
   return SIGB_OK;
 }
 
+extern "C" int sigb_jit_source(const uint64_t* codes, const int64_t* lengths, int64_t W, int64_t d, int dtype,
+                               int backward, char* buf, size_t cap, size_t* len) {
+  Trie t;
+  int rc = build_trie(codes, lengths, W, d, false, nullptr, t);
+  if (rc) return rc;
+  if (!jit::eligible(t)) return fail(SIGB_ERR_UNSUPPORTED, "word set too large for generated kernels");
+  JitHost h;
+  jit::make_plan(t, h);
+  const std::string src = jit::source(t, h, dtype, backward != 0);
+  if (len) *len = src.size();
+  if (buf && cap) {
+    const size_t n = std::min(cap - 1, src.size());
+    std::memcpy(buf, src.data(), n);
+    buf[n] = 0;
+  }
+  return SIGB_OK;
+}
+
 extern "C" int sigb_plan_create(const uint64_t* codes, const int64_t* lengths, int64_t W, int64_t d,
                                 sigb_plan** plan_out, void* stream_) {
   if (!plan_out) return fail(SIGB_ERR_DOMAIN, "plan output pointer is NULL");
@@ -320,6 +338,12 @@ extern "C" int sigb_plan_create(const uint64_t* codes, const int64_t* lengths, i
       fp.ok = true;
     }
   }
+  // word-set-specialised kernels (sigb_jit.cu): generated lazily, compiled on first use
+  if (jit::eligible(t)) {
+    plan->jit.eligible = true;
+    plan->jit.trie = t;
+    jit::make_plan(t, plan->jit.host);
+  }
   // level-slot plan (sigb_slot.cuh) for small sparse tries
   {
     SlotHost sh;
@@ -386,6 +410,9 @@ extern "C" int sigb_plan_destroy(sigb_plan* plan) {
   cudaFree(plan->frag.red_off);
   cudaFree(plan->slot.tinfo); cudaFree(plan->slot.meta0); cudaFree(plan->slot.meta1); cudaFree(plan->slot.pos);
   cudaFree(plan->slot.cidx); cudaFree(plan->slot.eidx); cudaFree(plan->slot.lvl); cudaFree(plan->slot.red_off);
+  for (auto& row : plan->jit.lib)
+    for (void* lib : row)
+      if (lib) cudaLibraryUnload((cudaLibrary_t)lib);
   delete plan;
   return SIGB_OK;
 }

@@ -99,3 +99,19 @@ def test_fragment_planner_random_sets():
         info = _lib.fragment_plan_info(ws.codes, ws.lengths, ws.d)
         closure = {w[:k] for w in words for k in range(1, len(w) + 1)}
         assert info["closure"] == len(closure)
+
+
+def test_generated_source_for_small_sets():
+    """The code generator (host-only) emits a kernel per direction with one case per task."""
+    import paper_2602_24066_b200 as sk
+    from tests.configs import build_wordset
+
+    ws = build_wordset("c3", sk)
+    fwd = _lib.jit_source(ws.codes, ws.lengths, ws.d, _lib.SIGB_F32, False)
+    bwd = _lib.jit_source(ws.codes, ws.lengths, ws.d, _lib.SIGB_F64, True)
+    assert 'extern "C" __global__' in fwd and "sigjit_fwd" in fwd and "typedef float R;" in fwd
+    assert "sigjit_bwd" in bwd and "typedef double R;" in bwd
+    assert fwd.count("case ") >= 2 and bwd.count("case ") >= fwd.count("case ")
+    with pytest.raises(_lib._ERRORS[4]):
+        big = build_wordset("c4", sk)
+        _lib.jit_source(big.codes, big.lengths, big.d, _lib.SIGB_F32, False)

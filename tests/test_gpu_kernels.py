@@ -2,7 +2,8 @@
 
 Kernel policies (sigb_set_kernel_policy): 0 = auto (truncated > slot or
 fragment > level), 1 = level-synchronous trie kernels, 2 = register-resident
-fragment kernels, 3 = level-slot kernels (small sparse tries).  Each family is checked against the C oracle (a restatement of the
+fragment kernels, 3 = level-slot kernels (small sparse tries), 4 = word-set
+specialised generated kernels (NVRTC).  Each family is checked against the C oracle (a restatement of the
 reference numba kernels pinned to the reference's golden vectors) and the
 golden vectors themselves, on the BASELINE configs' own word sets and on
 random tries (prefix-closed and not), with the north_star tolerances:
@@ -24,7 +25,7 @@ TOL64 = 1e-10
 TOL32 = 1e-4
 
 
-@pytest.fixture(params=[0, 1, 2, 3], ids=["auto", "level", "fragment", "slot"])
+@pytest.fixture(params=[0, 1, 2, 3, 4], ids=["auto", "level", "fragment", "slot", "generated"])
 def policy(request):
     _lib.set_kernel_policy(request.param)
     yield request.param
@@ -63,6 +64,8 @@ def check_set(ws, policy, B=3, L=12, seed=0):
         pytest.skip("no fragment shape for this set")
     if policy == 3 and plan.kernel_kind != 3:
         pytest.skip("set too large for one level-slot CTA")
+    if policy == 4 and plan.kernel_kind != 4:
+        pytest.skip("set too large for generated kernels")
     ref = ora.forward(X, ws.codes, ws.lengths, d)
     out = sk.signature_forward(X, ws).values
     assert ora.rel_err(out, ref) <= TOL64
@@ -93,7 +96,8 @@ def test_configs_every_family(golden_forward, golden_backward, policy, name):
 def test_auto_routing():
     kinds = {n: build_wordset(n, sk).plan().kernel_kind for n in CONFIGS}
     assert kinds["c1"] == kinds["c2"] == kinds["c5"] == 1  # truncated kernels
-    assert kinds["c3"] == kinds["c4"] == 2  # fragment kernels
+    assert kinds["c3"] == 4  # generated kernels (sparse 2,048-word set)
+    assert kinds["c4"] == 2  # fragment kernels
 
 
 @pytest.mark.parametrize("seed", range(6))

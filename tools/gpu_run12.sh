@@ -1,0 +1,9 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests/test_gpu_kernels.py -x -q > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.txt
+timeout 600 python bench.py --config c3 --no-e2e > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sigjit_bwd -c 1 \
+  -o gpurun_out/prof_c3_jbwd python bench.py --config c3 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --batch 1024 > gpurun_out/ncu_c3b.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sigjit_fwd -c 1 \
+  -o gpurun_out/prof_c3_jfwd python bench.py --config c3 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --batch 2048 > gpurun_out/ncu_c3f.log 2>&1
+echo done

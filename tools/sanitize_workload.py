@@ -44,7 +44,7 @@ def main():
         "aniso": sk.build_anisotropic(sk.AnisotropyWeights((1.0,) * 3 + (2.0,) * 3, 5.0)),
         "custom non-closed": sk.build_custom([(0, 1, 1), (1,), (2, 2, 2, 2), (3, 0)], 4),
     }
-    for policy in (0, 1, 2, 3):
+    for policy in (0, 1, 2, 3, 4):
         _lib.set_kernel_policy(policy)
         for name, ws in sets.items():
             run(ws, B=2 if "16" in name else 3, L=24 if "16" in name else 40)
