@@ -277,7 +277,8 @@ extern "C" int sigb_windows(const sigb_plan* plan, int dtype, const void* d_X, i
   if (use_trunc(plan))
     return trunc::forward(dtype, plan->d, plan->trunc_depth, d_X, B * K, L, d_bounds, K, d_out, plan->W, 0, 0,
                           (cudaStream_t)stream);
-  if (plan->frag.ok && (g_policy == 0 || g_policy == 2) && !use_trunc(plan))  // slot kernels have no windowed form
+  // level-slot / generated kernels have no windowed form: windows run on the fragment kernels
+  if (plan->frag.ok && g_policy != 1 && g_policy != 3 && !use_trunc(plan))
     return frag::forward(plan, dtype, d_X, B * K, L, d_bounds, K, d_out, plan->W, 0, 0, nullptr, (cudaStream_t)stream);
   if (dtype == SIGB_F32)
     return forward_t<float>(plan, d_X, B, L, d_bounds, K, d_out, plan->W, 0, 0, nullptr, nullptr, 0, 0,

@@ -126,6 +126,8 @@ struct JitPlan {
   void* kern[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   bool failed[2][2] = {{false, false}, {false, false}};
   bool broken = false;  // some compilation failed: route this plan elsewhere
+  int* counters = nullptr;  // per-group work counters of the persistent kernels (device)
+  int ncounters = 0;
 };
 namespace jit {
 bool eligible(const Trie& t);

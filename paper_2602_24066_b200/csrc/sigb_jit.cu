@@ -35,10 +35,10 @@
 namespace sigb {
 namespace jit {
 
-constexpr int kWarps = 8;     // tasks per CTA
+constexpr int kWarps = 4;     // tasks (warps) per CTA
 // steps staged per chunk / per CTA gradient reduction (fp64 halves both: smem)
-int chunk_steps(int dtype) { return dtype == SIGB_F32 ? 16 : 8; }
-int red_steps(int dtype) { return dtype == SIGB_F32 ? 4 : 2; }
+int chunk_steps(int dtype) { return dtype == SIGB_F32 ? 8 : 8; }
+int red_steps(int dtype) { return dtype == SIGB_F32 ? 2 : 2; }
 constexpr int kCapFwd = 96;   // T-nodes per task, forward
 constexpr int kCapBwd = 40;   // T-nodes per task, backward (adjoints double the live values)
 
@@ -102,6 +102,13 @@ std::vector<Task> make_tasks(const Trie& t, int64_t cap) {
   int64_t n1 = 0;
   while (n1 < Wc && t.len[n1] == 1) ++n1;
   visit(-1, {}, 0, n1);
+  // similar costs side by side: a CTA's warps wait for each other once per chunk
+  auto cost = [&](const Task& tk) {
+    int64_t c = 0;
+    for (int64_t u : tk.nodes) c += tnodes(t, u);
+    return c;
+  };
+  std::stable_sort(tasks.begin(), tasks.end(), [&](const Task& a, const Task& b) { return cost(a) > cost(b); });
   return tasks;
 }
 
@@ -182,22 +189,39 @@ std::string horner(const TaskView& v, int i, int m, const std::string& s, const 
 std::string common_head(int dtype, int d, bool backward) {
   std::ostringstream o;
   o << "typedef " << tname(dtype) << " R;\n";
-  o << "#define D " << d << "\n#define CH " << chunk_steps(dtype) << "\n";
+  o << "#define D " << d << "\n#define CH " << chunk_steps(dtype) << "\n#define WARPS " << kWarps << "\n";
   o << R"(
-// Stage samples [j0, j0+cs] of the CTA's 32 paths; Dl[s][z][lane] = increment.
-__device__ __forceinline__ void stage(const R* __restrict__ X, long long B, long long L, long long b0, int j0, int cs,
-                                      R* __restrict__ Xs, R* __restrict__ Dl) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+// Samples of the CTA's 32 paths are copied with cp.async into Xs; diff() turns
+// the landed chunk into Dl[s][z][lane] = increment, after which the next chunk's
+// copy is issued into Xs and overlaps the chunk's steps.
+#define PITCH ((CH + 1) * D + 1)
+__device__ __forceinline__ int smid() {
+  int s;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+  return s;
+}
+__device__ __forceinline__ void cp_async(R* dst, const R* src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  if (sizeof(R) == 4) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(src));
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void issue(const R* __restrict__ X, long long B, long long L, long long b0, int j0, int cs,
+                                      R* __restrict__ Xb) {
   const int rows = (cs + 1) * D;
-  for (int i = tid; i < 32 * rows; i += nt) {
+  for (int i = threadIdx.x; i < 32 * rows; i += blockDim.x) {
     const int p = i / rows, r = i % rows;
     const long long b = b0 + p;
-    Xs[p * ((CH + 1) * D + 1) + r] = b < B ? X[(b * L + j0) * D + r] : R(0);
+    if (b < B) cp_async(Xb + p * PITCH + r, X + (b * L + j0) * D + r);
+    else Xb[p * PITCH + r] = R(0);
   }
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+__device__ __forceinline__ void diff(const R* __restrict__ Xb, int cs, R* __restrict__ Dl) {
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
-  for (int i = tid; i < cs * D * 32; i += nt) {
+  for (int i = threadIdx.x; i < cs * D * 32; i += blockDim.x) {
     const int s = i / (D * 32), z = (i / 32) % D, p = i % 32;
-    const R* xs = Xs + p * ((CH + 1) * D + 1);
+    const R* xs = Xb + p * PITCH;
     Dl[i] = xs[(s + 1) * D + z] - xs[s * D + z];
   }
   __syncthreads();
@@ -210,32 +234,54 @@ __device__ __forceinline__ void stage(const R* __restrict__ X, long long B, long
 std::string gen_forward(const Trie& t, const std::vector<Task>& tasks, int dtype) {
   const int d = (int)t.d;
   std::ostringstream o;
-  o << common_head(dtype, d, false);
   o << R"(
-extern "C" __global__ void __launch_bounds__(256) sigjit_fwd(const R* __restrict__ X, long long B, long long L,
+extern "C" __global__ void __launch_bounds__(32 * WARPS) sigjit_fwd(const R* __restrict__ X, long long B, long long L,
     R* __restrict__ out, long long out_ld, long long out_col0, int include_empty, R* __restrict__ state,
-    long long Wc) {
+    long long Wc, int nblocks, int groups, int* __restrict__ counters) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  R* Xs = reinterpret_cast<R*>(smem_raw);
-  R* Dl = Xs + 32 * ((CH + 1) * D + 1);
-  const int lane = threadIdx.x & 31, task = blockIdx.y * 8 + (threadIdx.x >> 5);
-  const long long b0 = (long long)blockIdx.x * 32, b = b0 + lane;
+  R* Xs = reinterpret_cast<R*>(smem_raw);  // samples of the next chunk land here while Dl computes
+  R* Dl = Xs + 32 * PITCH;
+  const int lane = threadIdx.x & 31;
   const long long M = L - 1;
-  R* orow = out ? out + b * out_ld + out_col0 : nullptr;
-  R* srow = state ? state + b * Wc : nullptr;
-  const bool live = b < B;
-  if (orow && live && include_empty && task == 0) orow[-1] = R(1);
-  switch (task) {
+  // persistent CTAs pinned to a task group by SM: an SM's resident warps run the
+  // same few task bodies (instruction-cache locality); path blocks of a group are
+  // claimed through an atomic counter, then the CTA helps the other groups
+  __shared__ int work;
+  const int g0 = smid() % groups;
+  for (int pass = 0; pass < groups; ++pass) {
+   const int g = (g0 + pass) % groups;
+   for (;;) {
+    if (threadIdx.x == 0) work = atomicAdd(counters + g, 1);
+    __syncthreads();
+    const int pb = work;
+    __syncthreads();
+    if (pb >= nblocks) break;
+    const int task = g * WARPS + (threadIdx.x >> 5);
+    const long long b0 = (long long)pb * 32, b = b0 + lane;
+    R* orow = out ? out + b * out_ld + out_col0 : nullptr;
+    R* srow = state ? state + b * Wc : nullptr;
+    const bool live = b < B;
+    if (orow && live && include_empty && task == 0) orow[-1] = R(1);
+    switch (task) {
 )";
   std::vector<char> owned(t.code.size(), 0);
+  std::ostringstream fns;  // one __noinline__ function per task: registers are allocated per task
   for (size_t ti = 0; ti < tasks.size(); ++ti) {
     TaskView v(t, tasks[ti]);
     const int n = (int)tasks[ti].nodes.size();
-    o << "  case " << ti << ": {\n";
+    o << "  case " << ti << ": ftask_" << ti << "(X, B, L, M, b0, lane, live, orow, srow, Xs, Dl); break;\n";
+    std::ostringstream& o2 = fns;
+    o2 << "__device__ __noinline__ void ftask_" << ti << "(const R* __restrict__ X, long long B, long long L, "
+          "long long M, long long b0, int lane, bool live, R* __restrict__ orow, R* __restrict__ srow, "
+          "R* __restrict__ Xs, R* __restrict__ Dl) {\n";
+    {
+    std::ostringstream& o = o2;
     for (int i = 0; i < n; ++i) o << "    R s" << i << " = R(0);\n";
-    o << "    for (long long j0 = 0; j0 < M; j0 += CH) {\n";
+    o << "    if (M > 0) issue(X, B, L, b0, 0, (int)(M < CH ? M : CH), Xs);\n";
+    o << "    for (long long j0 = 0, c = 0; j0 < M; j0 += CH, ++c) {\n";
     o << "      const int cs = (int)(M - j0 < CH ? M - j0 : CH);\n";
-    o << "      stage(X, B, L, b0, (int)j0, cs, Xs, Dl);\n";
+    o << "      diff(Xs, cs, Dl);\n";
+    o << "      if (j0 + CH < M) issue(X, B, L, b0, (int)(j0 + CH), (int)(M - j0 - CH < CH ? M - j0 - CH : CH), Xs);\n";
     o << "      #pragma unroll 1\n      for (int s = 0; s < cs; ++s) {\n";
     o << "        const R* dr = Dl + s * D * 32 + lane;\n";
     emit_letters(o, v, dtype, "");
@@ -244,7 +290,7 @@ extern "C" __global__ void __launch_bounds__(256) sigjit_fwd(const R* __restrict
         o << "        const R t" << i << "_" << m << " = " << horner(v, i, m, "s" + std::to_string(i), "t") << ";\n";
       o << "        s" << i << " = " << horner(v, i, v.lvl[i], "s" + std::to_string(i), "t") << ";\n";
     }
-    o << "      }\n      __syncthreads();\n    }\n";
+    o << "      }\n    }\n";
     o << "    if (live) {\n";
     for (int i = 0; i < n; ++i) {
       const int64_t u = tasks[ti].nodes[i];
@@ -253,58 +299,83 @@ extern "C" __global__ void __launch_bounds__(256) sigjit_fwd(const R* __restrict
       if (t.emit[u] >= 0) o << "      if (orow) orow[" << t.emit[u] << "] = s" << i << ";\n";
       o << "      if (srow) srow[" << u << "] = s" << i << ";\n";
     }
-    o << "    }\n  } break;\n";
+    o << "    }\n}\n";
+    }
   }
-  o << "  default: {\n    const long long M2 = M;\n    for (long long j0 = 0; j0 < M2; j0 += CH) {\n"
-       "      stage(X, B, L, b0, (int)j0, (int)(M2 - j0 < CH ? M2 - j0 : CH), Xs, Dl);\n      __syncthreads();\n"
-       "    }\n  }\n  }\n}\n";
-  return o.str();
+  o << "  default: {\n    if (M > 0) issue(X, B, L, b0, 0, (int)(M < CH ? M : CH), Xs);\n"
+       "    for (long long j0 = 0, c = 0; j0 < M; j0 += CH, ++c) {\n"
+       "      diff(Xs, (int)(M - j0 < CH ? M - j0 : CH), Dl);\n"
+       "      if (j0 + CH < M) issue(X, B, L, b0, (int)(j0 + CH), (int)(M - j0 - CH < CH ? M - j0 - CH : CH), Xs);\n"
+       "    }\n  }\n    }\n   }\n  }\n}\n";
+  return common_head(dtype, d, false) + fns.str() + o.str();
 }
 
 std::string gen_backward(const Trie& t, const std::vector<Task>& tasks, int dtype) {
   const int d = (int)t.d;
-  std::ostringstream o;
-  o << common_head(dtype, d, true);
-  o << "#define KRED " << red_steps(dtype) << "\n";
-  o << R"(
+  std::ostringstream head, o;
+  head << common_head(dtype, d, true);
+  head << "#define KRED " << red_steps(dtype) << "\n";
+  head << R"(
 // Sum the 8 warps' parked gradients of the last `nr` steps (buffer slot r holds
 // step jlast - r) into partial[path][group][j][z], fixed order.
 __device__ __forceinline__ void flush(const R* __restrict__ G, int nr, long long jlast, long long B, long long b0,
-                                      long long M, R* __restrict__ partial, int groups) {
+                                      long long M, R* __restrict__ partial, int groups, int g) {
   __syncthreads();
   for (int i = threadIdx.x; i < nr * D * 32; i += blockDim.x) {
     const int r = i / (D * 32), z = (i / 32) % D, p = i % 32;
     R acc = R(0);
     #pragma unroll
-    for (int w = 0; w < 8; ++w) acc += G[((w * KRED + r) * D + z) * 32 + p];
+    for (int w = 0; w < WARPS; ++w) acc += G[((w * KRED + r) * D + z) * 32 + p];
     const long long b = b0 + p;
-    if (b < B) partial[((b * groups + blockIdx.y) * M + (jlast - r)) * D + z] = acc;
+    if (b < B) partial[((b * groups + g) * M + (jlast - r)) * D + z] = acc;
   }
   __syncthreads();
 }
-
-extern "C" __global__ void __launch_bounds__(256) sigjit_bwd(const R* __restrict__ X, long long B, long long L,
+)";
+  o << R"(
+extern "C" __global__ void __launch_bounds__(32 * WARPS) sigjit_bwd(const R* __restrict__ X, long long B, long long L,
     const R* __restrict__ Sin, long long s_ld, long long s_col0, const R* __restrict__ gup, long long g_ld,
-    long long g_col0, R* __restrict__ partial, int groups) {
+    long long g_col0, R* __restrict__ partial, int nblocks, int groups, int* __restrict__ counters) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  R* Xs = reinterpret_cast<R*>(smem_raw);
-  R* Dl = Xs + 32 * ((CH + 1) * D + 1);
-  R* Gb = Dl + CH * D * 32;  // [warp][KRED][D][32]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, task = blockIdx.y * 8 + warp;
-  const long long b0 = (long long)blockIdx.x * 32, b = b0 + lane;
-  const bool live = b < B;
-  const R* srow = Sin + (live ? b : 0) * s_ld + s_col0;
-  const R* grow = gup + (live ? b : 0) * g_ld + g_col0;
+  R* Xs = reinterpret_cast<R*>(smem_raw);  // samples of the next chunk land here while Dl computes
+  R* Dl = Xs + 32 * PITCH;
+  R* Gb = Dl + CH * D * 32;  // [warp][KRED][D][32], letters a task never touches stay 0
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long M = L - 1;
   R* gmine = Gb + warp * KRED * D * 32 + lane;
   const int nchunks = (int)((M + CH - 1) / CH);
-  switch (task) {
+  __shared__ int work;
+  const int g0 = smid() % groups;  // see sigjit_fwd: SM-pinned groups, then help the others
+  for (int pass = 0; pass < groups; ++pass) {
+   const int g = (g0 + pass) % groups;
+   __syncthreads();
+   for (int i = threadIdx.x; i < WARPS * KRED * D * 32; i += blockDim.x) Gb[i] = R(0);  // new tasks, new letters
+   for (;;) {
+    if (threadIdx.x == 0) work = atomicAdd(counters + g, 1);
+    __syncthreads();
+    const int pb = work;
+    __syncthreads();
+    if (pb >= nblocks) break;
+    const int task = g * WARPS + warp;
+    const long long b0 = (long long)pb * 32, b = b0 + lane;
+    const bool live = b < B;
+    const R* srow = Sin + (live ? b : 0) * s_ld + s_col0;
+    const R* grow = gup + (live ? b : 0) * g_ld + g_col0;
+    switch (task) {
 )";
   std::vector<char> owned(t.code.size(), 0);
+  std::ostringstream fns;  // one __noinline__ function per task
   for (size_t ti = 0; ti < tasks.size(); ++ti) {
     TaskView v(t, tasks[ti]);
     const int n = (int)tasks[ti].nodes.size();
-    o << "  case " << ti << ": {\n";
+    o << "  case " << ti << ": btask_" << ti
+      << "(X, B, L, M, b0, lane, live, srow, grow, Xs, Dl, Gb, gmine, partial, groups, g, nchunks); break;\n";
+    fns << "__device__ __noinline__ void btask_" << ti << "(const R* __restrict__ X, long long B, long long L, "
+           "long long M, long long b0, int lane, bool live, const R* __restrict__ srow, const R* __restrict__ grow, "
+           "R* __restrict__ Xs, R* __restrict__ Dl, R* __restrict__ Gb, R* __restrict__ gmine, "
+           "R* __restrict__ partial, int groups, int g, int nchunks) {\n";
+    {
+    std::ostringstream& o = fns;
     std::vector<char> own(n, 0);
     for (int i = 0; i < n; ++i) {
       const int64_t u = tasks[ti].nodes[i];
@@ -314,9 +385,11 @@ extern "C" __global__ void __launch_bounds__(256) sigjit_bwd(const R* __restrict
       if (own[i] && t.emit[u] >= 0) o << "    R l" << i << " = live ? grow[" << t.emit[u] << "] : R(0);\n";
       else o << "    R l" << i << " = R(0);\n";
     }
+    o << "    if (nchunks > 0) issue(X, B, L, b0, (nchunks - 1) * CH, (int)(M - (nchunks - 1) * CH), Xs);\n";
     o << "    for (int c = nchunks - 1; c >= 0; --c) {\n";
     o << "      const int j0 = c * CH;\n      const int cs = (int)(M - j0 < CH ? M - j0 : CH);\n";
-    o << "      stage(X, B, L, b0, j0, cs, Xs, Dl);\n      int nb = 0;\n";
+    o << "      diff(Xs, cs, Dl);\n";
+    o << "      if (c > 0) issue(X, B, L, b0, j0 - CH, CH, Xs);\n      int nb = 0;\n";
     o << "      #pragma unroll 1\n      for (int s = cs - 1; s >= 0; --s) {\n";
     o << "        const R* dr = Dl + s * D * 32 + lane;\n";
     emit_letters(o, v, dtype, "");
@@ -372,30 +445,30 @@ extern "C" __global__ void __launch_bounds__(256) sigjit_bwd(const R* __restrict
     // this step's lambda_{j+1} as its Tbar(u, |u|)
     for (int i = 0; i < n; ++i)
       for (int m = v.lvl[i] + 1; m <= v.mdt[i]; ++m) o << "        l" << i << " += b" << i << "_" << m << ";\n";
-    // (d) park this step's per-letter gradients (unused letters write 0)
-    for (int z = 0; z < d; ++z) {
-      auto it = gsum.find(z);
-      o << "        gmine[(nb * D + " << z << ") * 32] = " << (it == gsum.end() ? "R(0)" : it->second) << ";\n";
+    // (d) park this step's per-letter gradients (untouched letters stay 0)
+    for (auto& kv : gsum) o << "        gmine[(nb * D + " << kv.first << ") * 32] = " << kv.second << ";\n";
+    o << "        if (++nb == KRED || s == 0) { flush(Gb, nb, j0 + s + nb - 1, B, b0, M, partial, groups, g); nb = 0; }\n";
+    o << "      }\n    }\n}\n";
     }
-    o << "        if (++nb == KRED || s == 0) { flush(Gb, nb, j0 + s + nb - 1, B, b0, M, partial, groups); nb = 0; }\n";
-    o << "      }\n    }\n  } break;\n";
   }
   o << R"(  default: {
+    if (nchunks > 0) issue(X, B, L, b0, (nchunks - 1) * CH, (int)(M - (nchunks - 1) * CH), Xs);
     for (int c = nchunks - 1; c >= 0; --c) {
       const int j0 = c * CH;
       const int cs = (int)(M - j0 < CH ? M - j0 : CH);
-      stage(X, B, L, b0, j0, cs, Xs, Dl);
+      diff(Xs, cs, Dl);
+      if (c > 0) issue(X, B, L, b0, j0 - CH, CH, Xs);
       int nb = 0;
-      for (int s = cs - 1; s >= 0; --s) {
-        for (int z = 0; z < D; ++z) gmine[(nb * D + z) * 32] = R(0);
-        if (++nb == KRED || s == 0) { flush(Gb, nb, j0 + s + nb - 1, B, b0, M, partial, groups); nb = 0; }
-      }
+      for (int s = cs - 1; s >= 0; --s)
+        if (++nb == KRED || s == 0) { flush(Gb, nb, j0 + s + nb - 1, B, b0, M, partial, groups, g); nb = 0; }
     }
   }
+    }
+   }
   }
 }
 )";
-  return o.str();
+  return head.str() + fns.str() + o.str();
 }
 
 }  // namespace
@@ -510,20 +583,49 @@ int ensure(sigb_plan* p, int dtype, bool backward) {
   return SIGB_OK;
 }
 
+// Persistent grid: every SM filled once (the kernel claims path blocks itself).
+unsigned persistent_grid(const void* kern, size_t smem, int64_t work_items) {
+  int dev = 0, sms = 148, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kWarps, smem) != cudaSuccess || occ < 1) {
+    cudaGetLastError();
+    occ = 2;
+  }
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ, work_items));
+}
+
+int* counters(const sigb_plan* p, int n, cudaStream_t stream) {
+  JitPlan& J = const_cast<sigb_plan*>(p)->jit;
+  if (J.ncounters < n) {
+    if (J.counters) cudaFree(J.counters);
+    J.counters = nullptr;
+    if (cudaMalloc((void**)&J.counters, sizeof(int) * n) != cudaSuccess) return nullptr;
+    J.ncounters = n;
+  }
+  if (cudaMemsetAsync(J.counters, 0, sizeof(int) * n, stream) != cudaSuccess) return nullptr;
+  return J.counters;
+}
+
 int forward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, void* out, int64_t out_ld,
             int64_t out_col0, int include_empty, void* state, cudaStream_t stream) {
   if (B == 0) return SIGB_OK;
   int rc = ensure(const_cast<sigb_plan*>(p), dtype, false);
   if (rc) return rc;
   const int di = dtype == SIGB_F32 ? 0 : 1;
-  const int groups = (int)((p->jit.host.fwd_tasks.size() + kWarps - 1) / kWarps);
+  int groups = (int)((p->jit.host.fwd_tasks.size() + kWarps - 1) / kWarps);
+  int nblocks = (int)((B + 31) / 32);
+  int* ctr = counters(p, groups, stream);
+  if (!ctr) return fail(SIGB_ERR_CUDA, "work counters for the word-set kernel");
   long long Bl = B, Ll = L, ld = out_ld, c0 = out_col0, Wc = p->Wc;
   int inc = include_empty;
-  void* args[] = {(void*)&X, &Bl, &Ll, &out, &ld, &c0, &inc, &state, &Wc};
+  void* args[] = {(void*)&X, &Bl, &Ll, &out, &ld, &c0, &inc, &state, &Wc, &nblocks, &groups, &ctr};
+  const size_t smem = smem_bytes(dtype, (int)p->d, false);
+  const void* kern = (const void*)p->jit.kern[di][0];
   count_launch();
   timing_begin(0, stream);
-  SIGB_CUDA_TRY(cudaLaunchKernel((const void*)p->jit.kern[di][0], dim3((unsigned)((B + 31) / 32), groups),
-                                 dim3(32 * kWarps), args, smem_bytes(dtype, (int)p->d, false), stream));
+  SIGB_CUDA_TRY(cudaLaunchKernel(kern, dim3(persistent_grid(kern, smem, (int64_t)groups * nblocks)), dim3(32 * kWarps),
+                                 args, smem, stream));
   timing_end(0, stream);
   return SIGB_OK;
 }
@@ -587,12 +689,16 @@ int backward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L,
     void* Xv = (void*)Xc;
     void* Sv = (void*)Sc;
     void* gv = (void*)gc;
-    int grp = groups;
-    void* args[] = {&Xv, &Bl, &Ll, &Sv, &sl, &s0, &gv, &gl, &g0, &work, &grp};
+    int grp = groups, nblocks = (int)((Bc + 31) / 32);
+    int* ctr = counters(p, groups, stream);
+    if (!ctr) return fail(SIGB_ERR_CUDA, "work counters for the word-set kernel");
+    void* args[] = {&Xv, &Bl, &Ll, &Sv, &sl, &s0, &gv, &gl, &g0, &work, &nblocks, &grp, &ctr};
+    const size_t smem = smem_bytes(dtype, (int)d, true);
+    const void* kern = (const void*)p->jit.kern[di][1];
     count_launch(2);
     timing_begin(1, stream);
-    SIGB_CUDA_TRY(cudaLaunchKernel((const void*)p->jit.kern[di][1], dim3((unsigned)((Bc + 31) / 32), groups),
-                                   dim3(32 * kWarps), args, smem_bytes(dtype, (int)d, true), stream));
+    SIGB_CUDA_TRY(cudaLaunchKernel(kern, dim3(persistent_grid(kern, smem, (int64_t)groups * nblocks)),
+                                   dim3(32 * kWarps), args, smem, stream));
     timing_end(1, stream);
     const int64_t n = Bc * L * d;
     if (dtype == SIGB_F32)

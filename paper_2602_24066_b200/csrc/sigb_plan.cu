@@ -410,6 +410,7 @@ extern "C" int sigb_plan_destroy(sigb_plan* plan) {
   cudaFree(plan->frag.red_off);
   cudaFree(plan->slot.tinfo); cudaFree(plan->slot.meta0); cudaFree(plan->slot.meta1); cudaFree(plan->slot.pos);
   cudaFree(plan->slot.cidx); cudaFree(plan->slot.eidx); cudaFree(plan->slot.lvl); cudaFree(plan->slot.red_off);
+  cudaFree(plan->jit.counters);
   for (auto& row : plan->jit.lib)
     for (void* lib : row)
       if (lib) cudaLibraryUnload((cudaLibrary_t)lib);

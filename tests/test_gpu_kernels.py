@@ -214,8 +214,9 @@ def test_windows_every_family(policy, name):
     for k, o in enumerate(outs):
         assert ora.rel_err(o.values, ref[:, k]) <= TOL64, k
     # a whole-path window equals the forward signature bit for bit when both run the
-    # same kernel family (level-slot plans have no windowed form; windows use fragments)
-    if ws.plan().kernel_kind != 3:
+    # same kernel family (level-slot / generated plans have no windowed form; windows
+    # run on the fragment kernels)
+    if ws.plan().kernel_kind not in (3, 4):
         assert np.array_equal(outs[0].values, sk.signature_forward(X, ws).values)
     else:
         assert ora.rel_err(outs[0].values, sk.signature_forward(X, ws).values) <= TOL64
