@@ -113,9 +113,17 @@ struct Task {
   std::vector<int64_t> nodes;  // closure indices: chain (levels 1..c) then bodies, topological
   int chain = 0;               // leading chain nodes (replicated; the first task containing one owns it)
 };
+// Launch shape of one generated kernel: warps (= tasks) per slot, slots (path
+// blocks) per CTA, steps per staged chunk, minimum resident CTAs per SM
+// (register budget), T-node cap per task.
+struct Cfg {
+  int warps = 4, ch = 8, minb = 4, pb = 1;
+  int64_t cap = 96;
+};
 }  // namespace jit
 struct JitHost {
   std::vector<jit::Task> fwd_tasks, bwd_tasks;
+  jit::Cfg cfg[2][2];  // [dtype f32=0/f64=1][backward]
 };
 struct JitPlan {
   bool eligible = false;       // small enough for generated code

@@ -5,19 +5,26 @@
 //   - a task is a few sibling subtrees plus the chain of their common parent's
 //     ancestors; every node value, Horner partial and adjoint of the task is a
 //     named register in the generated code -- no shared-memory state, no
-//     barriers inside a step, no dead slots, and the scaled increments
-//     dX[z] / r are computed once per (letter, r) the task uses;
-//   - the 32 lanes of a warp run the same task for 32 paths, so the code is
-//     warp-uniform; increments are staged per chunk as [step][letter][lane].
+//     barriers inside a step, no dead slots; the 1/r of the Horner steps
+//     rides on the parent's partials (one scale per parent partial, shared
+//     by its children and the gradient terms), so a T-node is one FFMA;
+//   - the warps of a CTA run different tasks on the same 32 paths.  The CTA's
+//     samples arrive per chunk of CH steps by bulk copies (cp.async.bulk, one
+//     row of (CH+1)*D samples per path, completion on an mbarrier) and are
+//     differenced once into Dl[step][letter][lane] with vector loads, so every
+//     task reads an increment with one conflict-free LDS.
 // The fragment kernels (sigb_frag.cuh) pay ~24 issue slots of replicated
 // chain and dead letter slots per ~7 words on such sets; here every closure
 // node is one FMA per target per step.
 //
 // Backward: per step the task rebuilds its internal nodes
 // with -dX, recomputes their partials, runs reverse mode in reverse
-// topological order and accumulates dL/d(dX_j) per letter in lane registers;
-// the 8 warps (tasks) of a CTA are summed in shared memory in a fixed order
-// every kRed steps and the CTA groups of a path by the sample-grads epilogue.
+// topological order and accumulates dL/d(dX_j) per letter in lane registers
+// (one FFMA per T-node against the parent's scaled partial); each warp parks its per-letter
+// gradients of the chunk in shared memory and the CTA sums its warps in a
+// fixed order once per chunk, behind the barrier the chunk staging needs
+// anyway.  Partials [group][step][letter][path] are summed over groups and
+// telescoped into dL/dX by jit_sample_grads.
 #include <nvrtc.h>
 
 #include <algorithm>
@@ -35,14 +42,50 @@
 namespace sigb {
 namespace jit {
 
-constexpr int kWarps = 4;     // tasks (warps) per CTA
-// steps staged per chunk / per CTA gradient reduction (fp64 halves both: smem)
-int chunk_steps(int dtype) { return dtype == SIGB_F32 ? 8 : 8; }
-int red_steps(int dtype) { return dtype == SIGB_F32 ? 2 : 2; }
-constexpr int kCapFwd = 96;   // T-nodes per task, forward
-constexpr int kCapBwd = 40;   // T-nodes per task, backward (adjoints double the live values)
+size_t smem_bytes(int dtype, int d, const Cfg& c, bool backward);
 
 namespace {
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+
+// Defaults measured on B200 for config 3 (r01 sweeps, tools/jit_sweep.py):
+// the forward runs 3 slots x 4 tasks per SM (12 warps, 168 registers), the
+// backward 2 slots x 4 tasks (8 warps, up to 255 registers for 96-T-node
+// tasks).  Two slots of the same task on one SM scheduler share its
+// instruction cache; separate CTAs of different groups thrash it.
+// SIGB_JIT_* override the shape for sweeps; the chunk and slot counts then
+// shrink until the CTA fits in shared memory.
+Cfg default_cfg(int dtype, int d, bool backward) {
+  Cfg c;
+  if (!backward) {
+    c.warps = env_int("SIGB_JIT_FWARPS", 4);
+    c.ch = env_int("SIGB_JIT_FCH", 12);
+    c.minb = env_int("SIGB_JIT_FMINB", 1);
+    c.cap = env_int("SIGB_JIT_FCAP", 96);
+    c.pb = env_int("SIGB_JIT_FPB", 3);
+  } else {
+    c.warps = env_int("SIGB_JIT_BWARPS", 4);
+    c.ch = env_int("SIGB_JIT_BCH", 8);
+    c.minb = env_int("SIGB_JIT_BMINB", 1);
+    c.cap = env_int("SIGB_JIT_BCAP", 96);
+    c.pb = env_int("SIGB_JIT_BPB", 2);
+  }
+  c.warps = std::min(std::max(c.warps, 1), 16);
+  c.ch = std::min(std::max(c.ch, 1), 64);
+  c.minb = std::min(std::max(c.minb, 1), 16);
+  c.cap = std::max<int64_t>(c.cap, 1);
+  c.pb = std::min(std::max(c.pb, 1), 8);
+  c.warps = std::min(c.warps, 32 / c.pb);
+  constexpr size_t kSmemMax = 227 * 1024 - 1024;
+  while (smem_bytes(dtype, d, c, backward) > kSmemMax && (c.pb > 1 || c.ch > 1)) {
+    if (c.ch > 4 || c.pb == 1) c.ch = std::max(1, c.ch / 2);
+    else --c.pb;
+  }
+  return c;
+}
 
 int64_t tnodes(const Trie& t, int64_t u) { return t.md[u] - t.len[u] + 1; }
 
@@ -65,20 +108,18 @@ std::vector<Task> make_tasks(const Trie& t, int64_t cap) {
   const int64_t Wc = (int64_t)t.code.size();
   std::vector<int64_t> memo(Wc, -1);
   std::vector<Task> tasks;
-  std::function<void(int64_t, const std::vector<int64_t>&, int64_t, int64_t)> visit =
-      [&](int64_t parent, const std::vector<int64_t>& chain, int64_t cf, int64_t cc) {
+  std::function<void(const std::vector<int64_t>&, int64_t, int64_t)> visit =
+      [&](const std::vector<int64_t>& chain, int64_t cf, int64_t cc) {
         std::vector<int64_t> small;
         for (int64_t c = cf; c < cf + cc; ++c) {
           if (subtree_cost(t, c, memo) > cap && t.child_count[c] > 0) {
             std::vector<int64_t> ch2 = chain;
             ch2.push_back(c);
-            visit(c, ch2, t.child_first[c], t.child_count[c]);
+            visit(ch2, t.child_first[c], t.child_count[c]);
           } else {
             small.push_back(c);
           }
         }
-        (void)parent;
-        // chain cost: each chain node evaluates targets up to the deepest level below
         int64_t acc = 0;
         Task cur;
         auto flush = [&]() {
@@ -101,7 +142,7 @@ std::vector<Task> make_tasks(const Trie& t, int64_t cap) {
       };
   int64_t n1 = 0;
   while (n1 < Wc && t.len[n1] == 1) ++n1;
-  visit(-1, {}, 0, n1);
+  visit({}, 0, n1);
   // similar costs side by side: a CTA's warps wait for each other once per chunk
   auto cost = [&](const Task& tk) {
     int64_t c = 0;
@@ -132,7 +173,6 @@ struct TaskView {
   std::vector<int> par;         // local parent (-1: empty word)
   std::vector<int> lvl, mdt;    // level, deepest target within the task
   std::vector<std::vector<int>> kids;
-  std::set<std::pair<int, int>> scaled;  // (letter, r >= 2) used
   std::set<int> letters;
   TaskView(const Trie& t_, const Task& tk_) : t(t_), tk(tk_) {
     const int n = (int)tk.nodes.size();
@@ -153,210 +193,349 @@ struct TaskView {
       for (int c : kids[i]) m = std::max(m, mdt[c]);
       mdt[i] = m;
     }
-    for (int i = 0; i < n; ++i) {
-      const int z = letter(i);
-      letters.insert(z);
-      for (int r = 2; r <= mdt[i] - lvl[i] + 1; ++r) scaled.insert({z, r});
-    }
+    for (int i = 0; i < n; ++i) letters.insert(letter(i));
   }
   int letter(int i) const { return (int)(t.code[tk.nodes[i]] % (uint64_t)t.d); }
-  // factor dX[letter(i)] / r as an expression
-  std::string a(int i, int r) const {
-    const int z = letter(i);
-    return r == 1 ? "x" + std::to_string(z) : "x" + std::to_string(z) + "_" + std::to_string(r);
-  }
-  // T(parent(i), m) as an expression; T(eps, m) = 1
-  std::string tp(int i, int m, const char* pre) const {
-    if (par[i] < 0) return "";
-    return std::string(pre) + std::to_string(par[i]) + "_" + std::to_string(m);
+  std::string x(int i) const { return "x" + std::to_string(letter(i)); }
+  // P(parent(i), m) = T(parent(i), m) / (m - |parent(i)|), the factor of
+  // dX[letter(i)] in T(i, m) = dX[letter(i)] / (m - |i| + 1) * T(parent(i), m) + S(i):
+  // the 1/r of Alg. 1 moves onto the parent, one scale per parent partial
+  // shared by all its children (and by the gradient terms).  T(eps, m) = 1.
+  std::string pp(int i, int m, const char* pre, int dtype) const {
+    const int pi = par[i];
+    if (pi < 0) return lit(1.0 / m, dtype);
+    const std::string nm = std::string(pre) + std::to_string(pi) + "_" + std::to_string(m);
+    return m - lvl[pi] == 1 ? nm : "p" + nm;
   }
 };
 
-void emit_letters(std::ostringstream& o, const TaskView& v, int dtype, const char* sign) {
-  for (int z : v.letters) o << "        const R x" << z << " = " << sign << "dr[" << z << " * 32];\n";
-  for (auto& p : v.scaled)
-    o << "        const R x" << p.first << "_" << p.second << " = x" << p.first << " * " << lit(1.0 / p.second, dtype)
-      << ";\n";
+void emit_letters(std::ostringstream& o, const TaskView& v) {
+  for (int z : v.letters) o << "        const R x" << z << " = dr[" << z << " * 32];\n";
 }
 
-// T(u, m) = a * T(parent, m) + s  (parent eps: a + s)
-std::string horner(const TaskView& v, int i, int m, const std::string& s, const char* tpre) {
-  const std::string ai = v.a(i, m - v.lvl[i] + 1);
-  const std::string tpv = v.tp(i, m, tpre);
-  return tpv.empty() ? "(" + ai + " + " + s + ")" : "fma(" + ai + ", " + tpv + ", " + s + ")";
+// Partials T(i, m), m in (|i|, deepest], named <pre>i_m, and their scaled
+// copies p<pre>i_m for r = m - |i| >= 2; then S(i) <- T(i, |i|).  neg: the
+// group inverse exp(-dX) of the backward's reconstruction.
+void emit_node(std::ostringstream& o, const TaskView& v, int i, const char* pre, bool neg, bool update, int dtype) {
+  const std::string si = "s" + std::to_string(i), xi = (neg ? "-" : "") + v.x(i);
+  const int l = v.lvl[i];
+  if (!v.kids[i].empty())
+    for (int m = l + 1; m <= v.mdt[i]; ++m) {
+      const std::string nm = std::string(pre) + std::to_string(i) + "_" + std::to_string(m);
+      o << "        const R " << nm << " = fma(" << xi << ", " << v.pp(i, m, pre, dtype) << ", " << si << ");\n";
+      if (m - l >= 2) o << "        const R p" << nm << " = " << nm << " * " << lit(1.0 / (m - l), dtype) << ";\n";
+    }
+  if (update) o << "        " << si << " = fma(" << xi << ", " << v.pp(i, l, pre, dtype) << ", " << si << ");\n";
 }
 
-std::string common_head(int dtype, int d, bool backward) {
+double inv_fact(int k) {
+  double f = 1;
+  for (int i = 2; i <= k; ++i) f *= i;
+  return 1.0 / f;
+}
+
+// Backward form: Q(i, m) = T(i, m) / (m - |i|)!, so that
+//   Q(i, m) = dX[z_i] Q(parent, m) + S(i) / (m - |i|)!,   Q(eps, m) = 1 / m!,
+// and with the unscaled adjoints U(i, m) = (m - |i|)! Tbar(i, m),
+//   U(i, m) = sum_c dX[z_c] U(c, m),  U(i, |i|) = lambda(i),
+//   dL/dX[z] = sum over nodes u of letter z, m of U(u, m) Q(parent(u), m):
+// no scale on adjoint or gradient terms, one per state copy S(i) / k!, k >= 2.
+std::string qp(const TaskView& v, int i, int m, const char* pre, int dtype) {
+  const int pi = v.par[i];
+  if (pi < 0) return lit(inv_fact(m), dtype);
+  return std::string(pre) + std::to_string(pi) + "_" + std::to_string(m);
+}
+void emit_node_q(std::ostringstream& o, const TaskView& v, int i, const char* pre, bool neg, bool update, int dtype) {
+  const std::string si = "s" + std::to_string(i), xi = (neg ? "-" : "") + v.x(i);
+  const int l = v.lvl[i];
+  if (!v.kids[i].empty())
+    for (int m = l + 1; m <= v.mdt[i]; ++m) {
+      const std::string nm = std::string(pre) + std::to_string(i) + "_" + std::to_string(m);
+      std::string sc = si;
+      if (m - l >= 2) {
+        sc = "c" + nm;
+        o << "        const R " << sc << " = " << si << " * " << lit(inv_fact(m - l), dtype) << ";\n";
+      }
+      o << "        const R " << nm << " = fma(" << xi << ", " << qp(v, i, m, pre, dtype) << ", " << sc << ");\n";
+    }
+  if (update) o << "        " << si << " = fma(" << xi << ", " << qp(v, i, l, pre, dtype) << ", " << si << ");\n";
+}
+
+// Vector width of the staging loads/stores and the padded row pitch of the
+// sample buffer: rows start 16-byte aligned (bulk-copy destinations) and
+// PITCH / VW is odd, so a warp's vector loads of 32 rows hit distinct banks.
+int vec_width(int dtype, int d) {
+  if (dtype == SIGB_F32) return d % 4 == 0 ? 4 : d % 2 == 0 ? 2 : 1;
+  return d % 2 == 0 ? 2 : 1;
+}
+int pitch(int dtype, int d, int ch) {
+  const int es = dtype == SIGB_F32 ? 4 : 8;
+  const int al = 16 / es;  // elements per 16 bytes
+  int p = (ch + 1) * d;
+  p = (p + al - 1) / al * al;
+  const int vw = vec_width(dtype, d);
+  if ((p / vw) % 2 == 0) p += al;
+  return p;
+}
+
+std::string common_head(int dtype, int d, const Cfg& c) {
   std::ostringstream o;
+  const int vw = vec_width(dtype, d);
   o << "typedef " << tname(dtype) << " R;\n";
-  o << "#define D " << d << "\n#define CH " << chunk_steps(dtype) << "\n#define WARPS " << kWarps << "\n";
+  o << "#define D " << d << "\n#define CH " << c.ch << "\n#define WARPS " << c.warps << "\n#define NT (32 * WARPS)\n";
+  o << "#define PB " << c.pb << "\n";
+  o << "#define MINB " << c.minb << "\n#define VW " << vw << "\n#define PITCH " << pitch(dtype, d, c.ch) << "\n";
   o << R"(
-// Samples of the CTA's 32 paths are copied with cp.async into Xs; diff() turns
-// the landed chunk into Dl[s][z][lane] = increment, after which the next chunk's
-// copy is issued into Xs and overlaps the chunk's steps.
-#define PITCH ((CH + 1) * D + 1)
+struct __align__(VW * sizeof(R)) RV { R v[VW]; };
 __device__ __forceinline__ int smid() {
   int s;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
   return s;
 }
+__device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* m) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(m)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned phase) {
+  unsigned done;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(done) : "r"(su32(m)), "r"(phase) : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ int stid() { return (int)threadIdx.x % (32 * WARPS); }  // thread index in the slot
+__device__ __forceinline__ int slot_id() { return (int)(threadIdx.x >> 5) / WARPS; }
+__device__ __forceinline__ void slot_sync() {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + slot_id()), "r"(32 * WARPS) : "memory");
+}
 __device__ __forceinline__ void cp_async(R* dst, const R* src) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
-  if (sizeof(R) == 4) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(src));
-  else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
+  if (sizeof(R) == 4) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(su32(dst)), "l"(src) : "memory");
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(su32(dst)), "l"(src) : "memory");
 }
-__device__ __forceinline__ void issue(const R* __restrict__ X, long long B, long long L, long long b0, int j0, int cs,
-                                      R* __restrict__ Xb) {
+// Samples j0 .. j0+cs of the block's 32 paths -> Xs[p * PITCH + s * D + z].
+// bulk: one cp.async.bulk per path row (16-byte aligned rows), completion
+// counted in bytes on the mbarrier; otherwise element cp.async.
+__device__ __forceinline__ void issue(const R* __restrict__ X, long long B, long long L, long long b0, long long j0,
+                                      int cs, R* __restrict__ Xs, unsigned long long* mbar, int bulk) {
   const int rows = (cs + 1) * D;
-  for (int i = threadIdx.x; i < 32 * rows; i += blockDim.x) {
-    const int p = i / rows, r = i % rows;
-    const long long b = b0 + p;
-    if (b < B) cp_async(Xb + p * PITCH + r, X + (b * L + j0) * D + r);
-    else Xb[p * PITCH + r] = R(0);
+  const long long nl = B - b0 < 32 ? B - b0 : 32;
+  if (bulk) {
+    if (stid() < 32) {
+      const int p = stid();
+      if (p == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(mbar)),
+                     "r"((unsigned)(nl * rows * sizeof(R))) : "memory");
+      __syncwarp();
+      if (p < nl)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         su32(Xs + p * PITCH)), "l"(X + ((b0 + p) * L + j0) * D), "r"((unsigned)(rows * sizeof(R))),
+                     "r"(su32(mbar)) : "memory");
+    }
+  } else {
+    for (int p = stid() >> 5; p < nl; p += WARPS) {
+      const R* src = X + ((b0 + p) * L + j0) * D;
+      for (int r = stid() & 31; r < rows; r += 32) cp_async(Xs + p * PITCH + r, src + r);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  asm volatile("cp.async.commit_group;\n" ::);
 }
-__device__ __forceinline__ void diff(const R* __restrict__ Xb, int cs, R* __restrict__ Dl) {
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-  __syncthreads();
-  for (int i = threadIdx.x; i < cs * D * 32; i += blockDim.x) {
-    const int s = i / (D * 32), z = (i / 32) % D, p = i % 32;
-    const R* xs = Xb + p * PITCH;
-    Dl[i] = xs[(s + 1) * D + z] - xs[s * D + z];
+// Wait for the chunk issued last (every thread calls this once per chunk).
+__device__ __forceinline__ void land(unsigned long long* mbar, unsigned phase, int bulk) {
+  if (bulk) mbar_wait(mbar, phase);
+  else asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+// Dl[s][z][lane] = X[s+1][z] - X[s][z] for the lane's path.
+__device__ __forceinline__ void diff(const R* __restrict__ Xs, int cs, R* __restrict__ Dl) {
+  const int lane = threadIdx.x & 31;
+  const R* xs = Xs + lane * PITCH;
+  for (int it = stid() >> 5; it < cs * (D / VW); it += WARPS) {
+    const int s = it / (D / VW), q = it - s * (D / VW);
+    const RV a = *reinterpret_cast<const RV*>(xs + (s + 1) * D + q * VW);
+    const RV c = *reinterpret_cast<const RV*>(xs + s * D + q * VW);
+    R* dl = Dl + (s * D + q * VW) * 32 + lane;
+    #pragma unroll
+    for (int k = 0; k < VW; ++k) dl[k * 32] = a.v[k] - c.v[k];
   }
+}
+// A CTA is PB independent slots of WARPS warps (one path block each, own
+// named barrier, mbarrier and shared-memory region): the slots share an SM and
+// its task group -- the same task bodies in the instruction cache -- but never
+// wait for each other.
+__device__ __forceinline__ void cta_init(R* base, size_t elems, unsigned long long* mbar) {
+  if (threadIdx.x < PB) mbar_init(mbar + threadIdx.x);
+  for (size_t i = threadIdx.x; i < elems; i += blockDim.x) base[i] = R(0);  // rows of absent paths stay finite
   __syncthreads();
 }
 )";
-  (void)backward;
   return o.str();
 }
 
-std::string gen_forward(const Trie& t, const std::vector<Task>& tasks, int dtype) {
+std::string gen_forward(const Trie& t, const std::vector<Task>& tasks, int dtype, const Cfg& cfg) {
   const int d = (int)t.d;
-  std::ostringstream o;
+  std::ostringstream o, fns;
+  fns << R"(
+// Steps of the chunk loop shared by every task body (and the idle warps):
+// wait for the chunk, (A) all warps are done with the previous Dl, difference,
+// (B) Dl ready and Xs free, prefetch the next chunk into Xs.
+#define FWD_CHUNK_BEGIN                                                              \
+  const int cs = (int)(M - j0 < CH ? M - j0 : CH);                                   \
+  land(mbar, phase, bulk);                                                           \
+  phase ^= 1u;                                                                       \
+  slot_sync();                                                                       \
+  diff(Xs, cs, Dl);                                                                  \
+  slot_sync();                                                                       \
+  if (j0 + CH < M) issue(X, B, L, b0, j0 + CH, (int)(M - j0 - CH < CH ? M - j0 - CH : CH), Xs, mbar, bulk);
+__device__ __noinline__ void fidle(const R* __restrict__ X, long long B, long long L, long long M, long long b0,
+                                   R* __restrict__ Xs, R* __restrict__ Dl, unsigned long long* mbar, unsigned phase,
+                                   int bulk) {
+  if (M > 0) issue(X, B, L, b0, 0, (int)(M < CH ? M : CH), Xs, mbar, bulk);
+  for (long long j0 = 0; j0 < M; j0 += CH) { FWD_CHUNK_BEGIN }
+}
+)";
   o << R"(
-extern "C" __global__ void __launch_bounds__(32 * WARPS) sigjit_fwd(const R* __restrict__ X, long long B, long long L,
+extern "C" __global__ void __launch_bounds__(NT * PB, MINB) sigjit_fwd(const R* __restrict__ X, long long B, long long L,
     R* __restrict__ out, long long out_ld, long long out_col0, int include_empty, R* __restrict__ state,
-    long long Wc, int nblocks, int groups, int* __restrict__ counters) {
+    long long Wc, int nblocks, int groups, int* __restrict__ counters, int bulk) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  R* Xs = reinterpret_cast<R*>(smem_raw);  // samples of the next chunk land here while Dl computes
+  constexpr size_t SLOT = 32 * PITCH + CH * D * 32;
+  R* Xs = reinterpret_cast<R*>(smem_raw) + slot_id() * SLOT;
   R* Dl = Xs + 32 * PITCH;
+  __shared__ unsigned long long mbars[PB];
+  __shared__ int works[PB];
+  cta_init(reinterpret_cast<R*>(smem_raw), PB * SLOT, mbars);
+  unsigned long long* mbar = mbars + slot_id();
   const int lane = threadIdx.x & 31;
   const long long M = L - 1;
+  const unsigned nch = (unsigned)((M + CH - 1) / CH);
+  unsigned phase = 0;
   // persistent CTAs pinned to a task group by SM: an SM's resident warps run the
   // same few task bodies (instruction-cache locality); path blocks of a group are
-  // claimed through an atomic counter, then the CTA helps the other groups
-  __shared__ int work;
+  // claimed through an atomic counter, then the slot helps the other groups
   const int g0 = smid() % groups;
   for (int pass = 0; pass < groups; ++pass) {
    const int g = (g0 + pass) % groups;
    for (;;) {
-    if (threadIdx.x == 0) work = atomicAdd(counters + g, 1);
-    __syncthreads();
-    const int pb = work;
-    __syncthreads();
+    if (stid() == 0) works[slot_id()] = atomicAdd(counters + g, 1);
+    slot_sync();
+    const int pb = works[slot_id()];
+    slot_sync();
     if (pb >= nblocks) break;
-    const int task = g * WARPS + (threadIdx.x >> 5);
+    const int task = g * WARPS + (threadIdx.x >> 5) % WARPS;
     const long long b0 = (long long)pb * 32, b = b0 + lane;
-    R* orow = out ? out + b * out_ld + out_col0 : nullptr;
-    R* srow = state ? state + b * Wc : nullptr;
     const bool live = b < B;
-    if (orow && live && include_empty && task == 0) orow[-1] = R(1);
+    R* orow = out && live ? out + b * out_ld + out_col0 : nullptr;
+    R* srow = state && live ? state + b * Wc : nullptr;
+    if (orow && include_empty && task == 0) orow[-1] = R(1);
     switch (task) {
 )";
   std::vector<char> owned(t.code.size(), 0);
-  std::ostringstream fns;  // one __noinline__ function per task: registers are allocated per task
   for (size_t ti = 0; ti < tasks.size(); ++ti) {
     TaskView v(t, tasks[ti]);
     const int n = (int)tasks[ti].nodes.size();
-    o << "  case " << ti << ": ftask_" << ti << "(X, B, L, M, b0, lane, live, orow, srow, Xs, Dl); break;\n";
-    std::ostringstream& o2 = fns;
-    o2 << "__device__ __noinline__ void ftask_" << ti << "(const R* __restrict__ X, long long B, long long L, "
-          "long long M, long long b0, int lane, bool live, R* __restrict__ orow, R* __restrict__ srow, "
-          "R* __restrict__ Xs, R* __restrict__ Dl) {\n";
-    {
-    std::ostringstream& o = o2;
-    for (int i = 0; i < n; ++i) o << "    R s" << i << " = R(0);\n";
-    o << "    if (M > 0) issue(X, B, L, b0, 0, (int)(M < CH ? M : CH), Xs);\n";
-    o << "    for (long long j0 = 0, c = 0; j0 < M; j0 += CH, ++c) {\n";
-    o << "      const int cs = (int)(M - j0 < CH ? M - j0 : CH);\n";
-    o << "      diff(Xs, cs, Dl);\n";
-    o << "      if (j0 + CH < M) issue(X, B, L, b0, (int)(j0 + CH), (int)(M - j0 - CH < CH ? M - j0 - CH : CH), Xs);\n";
-    o << "      #pragma unroll 1\n      for (int s = 0; s < cs; ++s) {\n";
-    o << "        const R* dr = Dl + s * D * 32 + lane;\n";
-    emit_letters(o, v, dtype, "");
-    for (int i = 0; i < n; ++i) {
-      for (int m = v.lvl[i] + 1; m <= v.mdt[i]; ++m)
-        o << "        const R t" << i << "_" << m << " = " << horner(v, i, m, "s" + std::to_string(i), "t") << ";\n";
-      o << "        s" << i << " = " << horner(v, i, v.lvl[i], "s" + std::to_string(i), "t") << ";\n";
-    }
-    o << "      }\n    }\n";
-    o << "    if (live) {\n";
+    o << "  case " << ti << ": ftask_" << ti << "(X, B, L, M, b0, orow, srow, Xs, Dl, mbar, phase, bulk); break;\n";
+    fns << "__device__ __noinline__ void ftask_" << ti << "(const R* __restrict__ X, long long B, long long L, "
+           "long long M, long long b0, R* __restrict__ orow, R* __restrict__ srow, R* __restrict__ Xs, "
+           "R* __restrict__ Dl, unsigned long long* mbar, unsigned phase, int bulk) {\n";
+    fns << "  const int lane = threadIdx.x & 31;\n";
+    for (int i = 0; i < n; ++i) fns << "  R s" << i << " = R(0);\n";
+    fns << "  if (M > 0) issue(X, B, L, b0, 0, (int)(M < CH ? M : CH), Xs, mbar, bulk);\n";
+    fns << "  for (long long j0 = 0; j0 < M; j0 += CH) {\n    FWD_CHUNK_BEGIN\n";
+    fns << "    #pragma unroll 1\n    for (int s = 0; s < cs; ++s) {\n";
+    fns << "        const R* dr = Dl + s * D * 32 + lane;\n";
+    emit_letters(fns, v);
+    for (int i = 0; i < n; ++i) emit_node(fns, v, i, "t", false, true, dtype);
+    fns << "    }\n  }\n";
     for (int i = 0; i < n; ++i) {
       const int64_t u = tasks[ti].nodes[i];
       if (owned[u]) continue;
       owned[u] = 1;
-      if (t.emit[u] >= 0) o << "      if (orow) orow[" << t.emit[u] << "] = s" << i << ";\n";
-      o << "      if (srow) srow[" << u << "] = s" << i << ";\n";
+      if (t.emit[u] >= 0) fns << "  if (orow) orow[" << t.emit[u] << "] = s" << i << ";\n";
+      fns << "  if (srow) srow[" << u << "] = s" << i << ";\n";
     }
-    o << "    }\n}\n";
-    }
+    fns << "}\n";
   }
-  o << "  default: {\n    if (M > 0) issue(X, B, L, b0, 0, (int)(M < CH ? M : CH), Xs);\n"
-       "    for (long long j0 = 0, c = 0; j0 < M; j0 += CH, ++c) {\n"
-       "      diff(Xs, (int)(M - j0 < CH ? M - j0 : CH), Dl);\n"
-       "      if (j0 + CH < M) issue(X, B, L, b0, (int)(j0 + CH), (int)(M - j0 - CH < CH ? M - j0 - CH : CH), Xs);\n"
-       "    }\n  }\n    }\n   }\n  }\n}\n";
-  return common_head(dtype, d, false) + fns.str() + o.str();
+  o << "  default: fidle(X, B, L, M, b0, Xs, Dl, mbar, phase, bulk);\n    }\n    phase ^= nch & 1u;\n   }\n  }\n}\n";
+  return common_head(dtype, d, cfg) + fns.str() + o.str();
 }
 
-std::string gen_backward(const Trie& t, const std::vector<Task>& tasks, int dtype) {
+std::string gen_backward(const Trie& t, const std::vector<Task>& tasks, int dtype, const Cfg& cfg) {
   const int d = (int)t.d;
-  std::ostringstream head, o;
-  head << common_head(dtype, d, true);
-  head << "#define KRED " << red_steps(dtype) << "\n";
-  head << R"(
-// Sum the 8 warps' parked gradients of the last `nr` steps (buffer slot r holds
-// step jlast - r) into partial[path][group][j][z], fixed order.
-__device__ __forceinline__ void flush(const R* __restrict__ G, int nr, long long jlast, long long B, long long b0,
-                                      long long M, R* __restrict__ partial, int groups, int g) {
-  __syncthreads();
-  for (int i = threadIdx.x; i < nr * D * 32; i += blockDim.x) {
-    const int r = i / (D * 32), z = (i / 32) % D, p = i % 32;
-    R acc = R(0);
+  std::ostringstream fns, o;
+  fns << R"(
+// Sum the warps' parked gradients of one chunk (Gb[warp][s][z][lane], s local)
+// into partial[g][j0+s][z][path] (path pitch Bp), fixed warp order.
+__device__ __forceinline__ void reduce(const R* __restrict__ Gb, long long j0, int cs, R* __restrict__ partial,
+                                       long long Bp, long long M, int g, long long b0) {
+  for (int i = stid(); i < cs * D * (32 / VW); i += NT) {
+    const int q = i % (32 / VW), sz = i / (32 / VW);
+    RV acc = *reinterpret_cast<const RV*>(Gb + sz * 32 + q * VW);
     #pragma unroll
-    for (int w = 0; w < WARPS; ++w) acc += G[((w * KRED + r) * D + z) * 32 + p];
-    const long long b = b0 + p;
-    if (b < B) partial[((b * groups + g) * M + (jlast - r)) * D + z] = acc;
+    for (int w = 1; w < WARPS; ++w) {
+      const RV t = *reinterpret_cast<const RV*>(Gb + (w * CH * D + sz) * 32 + q * VW);
+      #pragma unroll
+      for (int k = 0; k < VW; ++k) acc.v[k] += t.v[k];
+    }
+    const int s = sz / D, z = sz - s * D;
+    *reinterpret_cast<RV*>(partial + (((long long)g * M + j0 + s) * D + z) * Bp + b0 + q * VW) = acc;
   }
-  __syncthreads();
+}
+// Chunk prologue of the reverse sweep (every warp, every chunk c = nch-1 .. 0):
+// wait for the chunk, (A) every warp is done with chunk c+1 -> sum its parked
+// gradients, difference chunk c, (B) Dl ready / Xs and Gb free, prefetch c-1.
+#define BWD_CHUNK_BEGIN                                                                     \
+  const long long j0 = (long long)c * CH;                                                   \
+  const int cs = (int)(M - j0 < CH ? M - j0 : CH);                                          \
+  land(mbar, phase, bulk);                                                                  \
+  phase ^= 1u;                                                                              \
+  slot_sync();                                                                              \
+  if (c + 1 < nch) reduce(Gb, j0 + CH, (int)(M - j0 - CH < CH ? M - j0 - CH : CH), partial, Bp, M, g, b0); \
+  diff(Xs, cs, Dl);                                                                         \
+  slot_sync();                                                                              \
+  if (c > 0) issue(X, B, L, b0, j0 - CH, CH, Xs, mbar, bulk);
+#define BWD_PROLOGUE                                                                        \
+  const int nch = (int)((M + CH - 1) / CH);                                                 \
+  if (nch > 0) issue(X, B, L, b0, (long long)(nch - 1) * CH, (int)(M - (long long)(nch - 1) * CH), Xs, mbar, bulk);
+#define BWD_EPILOGUE                                                                        \
+  slot_sync();                                                                              \
+  if (nch > 0) reduce(Gb, 0, (int)(M < CH ? M : CH), partial, Bp, M, g, b0);
+__device__ __noinline__ void bidle(const R* __restrict__ X, long long B, long long L, long long M, long long b0,
+                                   R* __restrict__ Xs, R* __restrict__ Dl, R* __restrict__ Gb, R* __restrict__ partial,
+                                   long long Bp, int g, unsigned long long* mbar, unsigned phase, int bulk) {
+  BWD_PROLOGUE
+  for (int c = nch - 1; c >= 0; --c) { BWD_CHUNK_BEGIN }
+  BWD_EPILOGUE
 }
 )";
   o << R"(
-extern "C" __global__ void __launch_bounds__(32 * WARPS) sigjit_bwd(const R* __restrict__ X, long long B, long long L,
+extern "C" __global__ void __launch_bounds__(NT * PB, MINB) sigjit_bwd(const R* __restrict__ X, long long B, long long L,
     const R* __restrict__ Sin, long long s_ld, long long s_col0, const R* __restrict__ gup, long long g_ld,
-    long long g_col0, R* __restrict__ partial, int nblocks, int groups, int* __restrict__ counters) {
+    long long g_col0, R* __restrict__ partial, long long Bp, int nblocks, int groups, int* __restrict__ counters,
+    int bulk) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  R* Xs = reinterpret_cast<R*>(smem_raw);  // samples of the next chunk land here while Dl computes
+  constexpr size_t SLOT = 32 * PITCH + CH * D * 32 + WARPS * CH * D * 32;
+  R* Xs = reinterpret_cast<R*>(smem_raw) + slot_id() * SLOT;
   R* Dl = Xs + 32 * PITCH;
-  R* Gb = Dl + CH * D * 32;  // [warp][KRED][D][32], letters a task never touches stay 0
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  R* Gb = Dl + CH * D * 32;  // [warp][CH][D][32]; letters a task never touches stay 0
+  __shared__ unsigned long long mbars[PB];
+  __shared__ int works[PB];
+  cta_init(reinterpret_cast<R*>(smem_raw), PB * SLOT, mbars);
+  unsigned long long* mbar = mbars + slot_id();
+  const int lane = threadIdx.x & 31;
   const long long M = L - 1;
-  R* gmine = Gb + warp * KRED * D * 32 + lane;
-  const int nchunks = (int)((M + CH - 1) / CH);
-  __shared__ int work;
+  const unsigned nch = (unsigned)((M + CH - 1) / CH);
+  unsigned phase = 0;
   const int g0 = smid() % groups;  // see sigjit_fwd: SM-pinned groups, then help the others
   for (int pass = 0; pass < groups; ++pass) {
    const int g = (g0 + pass) % groups;
-   __syncthreads();
-   for (int i = threadIdx.x; i < WARPS * KRED * D * 32; i += blockDim.x) Gb[i] = R(0);  // new tasks, new letters
+   slot_sync();
+   for (int i = stid(); i < WARPS * CH * D * 32; i += NT) Gb[i] = R(0);  // new tasks, new letters
    for (;;) {
-    if (threadIdx.x == 0) work = atomicAdd(counters + g, 1);
-    __syncthreads();
-    const int pb = work;
-    __syncthreads();
+    if (stid() == 0) works[slot_id()] = atomicAdd(counters + g, 1);
+    slot_sync();
+    const int pb = works[slot_id()];
+    slot_sync();
     if (pb >= nblocks) break;
-    const int task = g * WARPS + warp;
+    const int task = g * WARPS + (threadIdx.x >> 5) % WARPS;
     const long long b0 = (long long)pb * 32, b = b0 + lane;
     const bool live = b < B;
     const R* srow = Sin + (live ? b : 0) * s_ld + s_col0;
@@ -364,111 +543,77 @@ extern "C" __global__ void __launch_bounds__(32 * WARPS) sigjit_bwd(const R* __r
     switch (task) {
 )";
   std::vector<char> owned(t.code.size(), 0);
-  std::ostringstream fns;  // one __noinline__ function per task
   for (size_t ti = 0; ti < tasks.size(); ++ti) {
     TaskView v(t, tasks[ti]);
     const int n = (int)tasks[ti].nodes.size();
     o << "  case " << ti << ": btask_" << ti
-      << "(X, B, L, M, b0, lane, live, srow, grow, Xs, Dl, Gb, gmine, partial, groups, g, nchunks); break;\n";
+      << "(X, B, L, M, b0, live, srow, grow, Xs, Dl, Gb, partial, Bp, g, mbar, phase, bulk); break;\n";
     fns << "__device__ __noinline__ void btask_" << ti << "(const R* __restrict__ X, long long B, long long L, "
-           "long long M, long long b0, int lane, bool live, const R* __restrict__ srow, const R* __restrict__ grow, "
-           "R* __restrict__ Xs, R* __restrict__ Dl, R* __restrict__ Gb, R* __restrict__ gmine, "
-           "R* __restrict__ partial, int groups, int g, int nchunks) {\n";
-    {
-    std::ostringstream& o = fns;
+           "long long M, long long b0, bool live, const R* __restrict__ srow, const R* __restrict__ grow, "
+           "R* __restrict__ Xs, R* __restrict__ Dl, R* __restrict__ Gb, R* __restrict__ partial, long long Bp, "
+           "int g, unsigned long long* mbar, unsigned phase, int bulk) {\n";
+    fns << "  const int lane = threadIdx.x & 31;\n";
+    fns << "  R* gmine = Gb + ((threadIdx.x >> 5) % WARPS) * CH * D * 32 + lane;\n";
     std::vector<char> own(n, 0);
     for (int i = 0; i < n; ++i) {
       const int64_t u = tasks[ti].nodes[i];
       if (!owned[u]) { owned[u] = 1; own[i] = 1; }
-      const bool internal = !v.kids[i].empty();
-      if (internal) o << "    R s" << i << " = live ? srow[" << u << "] : R(0);\n";
-      if (own[i] && t.emit[u] >= 0) o << "    R l" << i << " = live ? grow[" << t.emit[u] << "] : R(0);\n";
-      else o << "    R l" << i << " = R(0);\n";
+      if (!v.kids[i].empty()) fns << "  R s" << i << " = live ? srow[" << u << "] : R(0);\n";
+      if (own[i] && t.emit[u] >= 0) fns << "  R l" << i << " = live ? grow[" << t.emit[u] << "] : R(0);\n";
+      else fns << "  R l" << i << " = R(0);\n";
     }
-    o << "    if (nchunks > 0) issue(X, B, L, b0, (nchunks - 1) * CH, (int)(M - (nchunks - 1) * CH), Xs);\n";
-    o << "    for (int c = nchunks - 1; c >= 0; --c) {\n";
-    o << "      const int j0 = c * CH;\n      const int cs = (int)(M - j0 < CH ? M - j0 : CH);\n";
-    o << "      diff(Xs, cs, Dl);\n";
-    o << "      if (c > 0) issue(X, B, L, b0, j0 - CH, CH, Xs);\n      int nb = 0;\n";
-    o << "      #pragma unroll 1\n      for (int s = cs - 1; s >= 0; --s) {\n";
-    o << "        const R* dr = Dl + s * D * 32 + lane;\n";
-    emit_letters(o, v, dtype, "");
-    // (a) rebuild internal nodes with -dX: tm partials from the parent's tm
-    for (int i = 0; i < n; ++i) {
-      if (v.kids[i].empty()) continue;
-      const std::string si = "s" + std::to_string(i);
-      for (int m = v.lvl[i] + 1; m <= v.mdt[i]; ++m) {
-        const std::string ai = v.a(i, m - v.lvl[i] + 1), tpv = v.tp(i, m, "q");
-        o << "        const R q" << i << "_" << m << " = "
-          << (tpv.empty() ? "(" + si + " - " + ai + ")" : "fma(-" + ai + ", " + tpv + ", " + si + ")") << ";\n";
-      }
-      const std::string ai = v.a(i, 1), tpv = v.tp(i, v.lvl[i], "q");
-      o << "        " << si << " = " << (tpv.empty() ? "(" + si + " - " + ai + ")" : "fma(-" + ai + ", " + tpv + ", " + si + ")")
-        << ";\n";
-    }
+    fns << "  BWD_PROLOGUE\n";
+    fns << "  for (int c = nch - 1; c >= 0; --c) {\n    BWD_CHUNK_BEGIN\n";
+    fns << "    #pragma unroll 1\n    for (int s = cs - 1; s >= 0; --s) {\n";
+    fns << "        const R* dr = Dl + s * D * 32 + lane;\n";
+    emit_letters(fns, v);
+    // (a) rebuild internal nodes with -dX (S_{0,t_j} = S_{0,t_j+1} (x) exp(-dX_j)), top-down
+    for (int i = 0; i < n; ++i)
+      if (!v.kids[i].empty()) emit_node_q(fns, v, i, "q", true, true, dtype);
     // (b) forward partials from S_{0,t_j}
-    for (int i = 0; i < n; ++i) {
-      if (v.kids[i].empty()) continue;
-      for (int m = v.lvl[i] + 1; m <= v.mdt[i]; ++m)
-        o << "        const R t" << i << "_" << m << " = " << horner(v, i, m, "s" + std::to_string(i), "t") << ";\n";
-    }
-    // (c) reverse, children before parents
-    std::map<int, std::string> gsum;  // letter -> expression list
+    for (int i = 0; i < n; ++i)
+      if (!v.kids[i].empty()) emit_node_q(fns, v, i, "t", false, false, dtype);
+    // (c) reverse, children before parents (U form, see emit_node_q)
+    std::set<int> gstarted;
     for (int i = n - 1; i >= 0; --i) {
       const int l = v.lvl[i];
       const std::string li = "l" + std::to_string(i);
-      // Tbar(i, m), m > l, from the children: sum a(c, m - l) * Tbar(c, m)
       for (int m = l + 1; m <= v.mdt[i]; ++m) {
         std::string e;
         for (int c : v.kids[i]) {
           if (v.mdt[c] < m) continue;
           const std::string tbc = m == v.lvl[c] ? "l" + std::to_string(c) : "b" + std::to_string(c) + "_" + std::to_string(m);
-          const std::string ac = v.a(c, m - v.lvl[c] + 1);
-          e = e.empty() ? ac + " * " + tbc : "fma(" + ac + ", " + tbc + ", " + e + ")";
+          e = e.empty() ? v.x(c) + " * " + tbc : "fma(" + v.x(c) + ", " + tbc + ", " + e + ")";
         }
-        o << "        const R b" << i << "_" << m << " = " << (e.empty() ? "R(0)" : e) << ";\n";
-      }
-      // gradient term for letter(i): sum_m Tbar(i, m) T(parent, m) / (m - l + 1)
-      std::string g;
-      for (int m = l; m <= v.mdt[i]; ++m) {
-        const std::string tb = m == l ? li : "b" + std::to_string(i) + "_" + std::to_string(m);
-        const std::string tpv = v.tp(i, m, "t");
-        const std::string w = m == l ? tb : tb + " * " + lit(1.0 / (m - l + 1), dtype);
-        g = g.empty() ? (tpv.empty() ? w : w + " * " + tpv)
-                      : (tpv.empty() ? "(" + g + " + " + w + ")" : "fma(" + w + ", " + tpv + ", " + g + ")");
+        fns << "        const R b" << i << "_" << m << " = " << e << ";\n";
       }
       const int z = v.letter(i);
-      o << "        const R g" << i << " = " << g << ";\n";
-      gsum[z] = gsum[z].empty() ? "g" + std::to_string(i) : gsum[z] + " + g" + std::to_string(i);
+      const std::string G = "G" + std::to_string(z);
+      for (int m = l; m <= v.mdt[i]; ++m) {
+        const std::string tb = m == l ? li : "b" + std::to_string(i) + "_" + std::to_string(m);
+        const std::string P = qp(v, i, m, "t", dtype);
+        if (!gstarted.count(z)) {
+          gstarted.insert(z);
+          fns << "        R " << G << " = " << tb << " * " << P << ";\n";
+        } else {
+          fns << "        " << G << " = fma(" << tb << ", " << P << ", " << G << ");\n";
+        }
+      }
     }
     // adjoints of the node values for the previous step, after every node used
     // this step's lambda_{j+1} as its Tbar(u, |u|)
     for (int i = 0; i < n; ++i)
-      for (int m = v.lvl[i] + 1; m <= v.mdt[i]; ++m) o << "        l" << i << " += b" << i << "_" << m << ";\n";
-    // (d) park this step's per-letter gradients (untouched letters stay 0)
-    for (auto& kv : gsum) o << "        gmine[(nb * D + " << kv.first << ") * 32] = " << kv.second << ";\n";
-    o << "        if (++nb == KRED || s == 0) { flush(Gb, nb, j0 + s + nb - 1, B, b0, M, partial, groups, g); nb = 0; }\n";
-    o << "      }\n    }\n}\n";
-    }
+      for (int m = v.lvl[i] + 1; m <= v.mdt[i]; ++m) {
+        if (m - v.lvl[i] == 1) fns << "        l" << i << " += b" << i << "_" << m << ";\n";
+        else fns << "        l" << i << " = fma(b" << i << "_" << m << ", " << lit(inv_fact(m - v.lvl[i]), dtype) << ", l" << i << ");\n";
+      }
+    // (d) park dL/d(dX_j) for the chunk reduction
+    for (int z : gstarted) fns << "        gmine[(s * D + " << z << ") * 32] = G" << z << ";\n";
+    fns << "    }\n  }\n  BWD_EPILOGUE\n}\n";
   }
-  o << R"(  default: {
-    if (nchunks > 0) issue(X, B, L, b0, (nchunks - 1) * CH, (int)(M - (nchunks - 1) * CH), Xs);
-    for (int c = nchunks - 1; c >= 0; --c) {
-      const int j0 = c * CH;
-      const int cs = (int)(M - j0 < CH ? M - j0 : CH);
-      diff(Xs, cs, Dl);
-      if (c > 0) issue(X, B, L, b0, j0 - CH, CH, Xs);
-      int nb = 0;
-      for (int s = cs - 1; s >= 0; --s)
-        if (++nb == KRED || s == 0) { flush(Gb, nb, j0 + s + nb - 1, B, b0, M, partial, groups, g); nb = 0; }
-    }
-  }
-    }
-   }
-  }
-}
-)";
-  return head.str() + fns.str() + o.str();
+  o << "  default: bidle(X, B, L, M, b0, Xs, Dl, Gb, partial, Bp, g, mbar, phase, bulk);\n"
+       "    }\n    phase ^= nch & 1u;\n   }\n  }\n}\n";
+  return common_head(dtype, d, cfg) + fns.str() + o.str();
 }
 
 }  // namespace
@@ -481,25 +626,27 @@ bool eligible(const Trie& t) {
   return Wc >= 2 && Wc <= 4096 && t.max_len <= 8 && t.d <= 32;
 }
 
-// Task cuts for the forward and the backward of a closure.
+// Task cuts and launch shapes for the forward and the backward of a closure.
 void make_plan(const Trie& t, JitHost& h) {
-  h.fwd_tasks = make_tasks(t, kCapFwd);
-  h.bwd_tasks = make_tasks(t, kCapBwd);
+  for (int di = 0; di < 2; ++di)
+    for (int bi = 0; bi < 2; ++bi) h.cfg[di][bi] = default_cfg(di == 0 ? SIGB_F32 : SIGB_F64, (int)t.d, bi == 1);
+  h.fwd_tasks = make_tasks(t, h.cfg[0][0].cap);
+  h.bwd_tasks = make_tasks(t, h.cfg[0][1].cap);
 }
 
 std::string source(const Trie& t, const JitHost& h, int dtype, bool backward) {
-  return backward ? gen_backward(t, h.bwd_tasks, dtype) : gen_forward(t, h.fwd_tasks, dtype);
+  const Cfg& c = h.cfg[dtype == SIGB_F32 ? 0 : 1][backward ? 1 : 0];
+  return backward ? gen_backward(t, h.bwd_tasks, dtype, c) : gen_forward(t, h.fwd_tasks, dtype, c);
+}
+
+size_t smem_bytes(int dtype, int d, const Cfg& c, bool backward) {
+  const size_t es = dtype == SIGB_F32 ? 4 : 8;
+  size_t n = 32 * (size_t)pitch(dtype, d, c.ch) + (size_t)c.ch * d * 32;
+  if (backward) n += (size_t)c.warps * c.ch * d * 32;
+  return n * es * c.pb;
 }
 
 namespace {
-
-size_t smem_bytes(int dtype, int d, bool backward) {
-  const size_t es = dtype == SIGB_F32 ? 4 : 8;
-  const int ch = chunk_steps(dtype), kr = red_steps(dtype);
-  size_t n = 32 * ((size_t)(ch + 1) * d + 1) + (size_t)ch * d * 32;
-  if (backward) n += (size_t)kWarps * kr * d * 32;
-  return n * es;
-}
 
 std::string cache_dir() {
   if (const char* e = getenv("SIGB_JIT_CACHE")) return e;
@@ -529,8 +676,8 @@ int compile(const std::string& src, std::string& cubin) {
   nvrtcProgram prog;
   if (nvrtcCreateProgram(&prog, src.c_str(), "sigb_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
     return fail(SIGB_ERR_CUDA, "nvrtcCreateProgram failed");
-  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-default-device", "--use_fast_math=false"};
-  nvrtcResult rc = nvrtcCompileProgram(prog, 3, opts);
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-default-device", "-lineinfo"};
+  nvrtcResult rc = nvrtcCompileProgram(prog, 4, opts);
   if (rc != NVRTC_SUCCESS) {
     size_t n = 0;
     nvrtcGetProgramLogSize(prog, &n);
@@ -554,6 +701,10 @@ int compile(const std::string& src, std::string& cubin) {
   return SIGB_OK;
 }
 
+const Cfg& cfg_of(const sigb_plan* p, int dtype, bool backward) {
+  return p->jit.host.cfg[dtype == SIGB_F32 ? 0 : 1][backward ? 1 : 0];
+}
+
 }  // namespace
 
 int ensure(sigb_plan* p, int dtype, bool backward) {
@@ -573,7 +724,7 @@ int ensure(sigb_plan* p, int dtype, bool backward) {
   if (e == cudaSuccess) e = cudaLibraryGetKernel(&kern, lib, backward ? "sigjit_bwd" : "sigjit_fwd");
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem_bytes(dtype, (int)p->d, backward));
+                             (int)smem_bytes(dtype, (int)p->d, cfg_of(p, dtype, backward), backward));
   if (e != cudaSuccess) {
     J.failed[di][bi] = J.broken = true;
     return cuda_fail(e, "loading the word-set kernel");
@@ -583,14 +734,16 @@ int ensure(sigb_plan* p, int dtype, bool backward) {
   return SIGB_OK;
 }
 
+namespace {
+
 // Persistent grid: every SM filled once (the kernel claims path blocks itself).
-unsigned persistent_grid(const void* kern, size_t smem, int64_t work_items) {
+unsigned persistent_grid(const void* kern, int threads, size_t smem, int64_t work_items) {
   int dev = 0, sms = 148, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kWarps, smem) != cudaSuccess || occ < 1) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess || occ < 1) {
     cudaGetLastError();
-    occ = 2;
+    occ = 1;
   }
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ, work_items));
 }
@@ -607,66 +760,116 @@ int* counters(const sigb_plan* p, int n, cudaStream_t stream) {
   return J.counters;
 }
 
+// Bulk copies need 16-byte aligned rows: D * sizeof(R) and the base pointer.
+int bulk_ok(const void* X, int dtype, int64_t d) {
+  const size_t es = dtype == SIGB_F32 ? 4 : 8;
+  return ((uintptr_t)X % 16 == 0 && (d * es) % 16 == 0) ? 1 : 0;
+}
+
+}  // namespace
+
 int forward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, void* out, int64_t out_ld,
             int64_t out_col0, int include_empty, void* state, cudaStream_t stream) {
   if (B == 0) return SIGB_OK;
   int rc = ensure(const_cast<sigb_plan*>(p), dtype, false);
   if (rc) return rc;
   const int di = dtype == SIGB_F32 ? 0 : 1;
-  int groups = (int)((p->jit.host.fwd_tasks.size() + kWarps - 1) / kWarps);
+  const Cfg& c = cfg_of(p, dtype, false);
+  int groups = (int)((p->jit.host.fwd_tasks.size() + c.warps - 1) / c.warps);
   int nblocks = (int)((B + 31) / 32);
   int* ctr = counters(p, groups, stream);
   if (!ctr) return fail(SIGB_ERR_CUDA, "work counters for the word-set kernel");
   long long Bl = B, Ll = L, ld = out_ld, c0 = out_col0, Wc = p->Wc;
-  int inc = include_empty;
-  void* args[] = {(void*)&X, &Bl, &Ll, &out, &ld, &c0, &inc, &state, &Wc, &nblocks, &groups, &ctr};
-  const size_t smem = smem_bytes(dtype, (int)p->d, false);
+  int inc = include_empty, bulk = bulk_ok(X, dtype, p->d);
+  void* args[] = {(void*)&X, &Bl, &Ll, &out, &ld, &c0, &inc, &state, &Wc, &nblocks, &groups, &ctr, &bulk};
+  const size_t smem = smem_bytes(dtype, (int)p->d, c, false);
   const void* kern = (const void*)p->jit.kern[di][0];
   count_launch();
   timing_begin(0, stream);
-  SIGB_CUDA_TRY(cudaLaunchKernel(kern, dim3(persistent_grid(kern, smem, (int64_t)groups * nblocks)), dim3(32 * kWarps),
-                                 args, smem, stream));
+  const int threads = 32 * c.warps * c.pb;
+  SIGB_CUDA_TRY(cudaLaunchKernel(kern, dim3(persistent_grid(kern, threads, smem, ((int64_t)groups * nblocks + c.pb - 1) / c.pb)),
+                                 dim3(threads), args, smem, stream));
   timing_end(0, stream);
   return SIGB_OK;
 }
 
 namespace {
 constexpr size_t kPartialBudget = size_t(4) << 30;
+constexpr int kTT = 16;  // samples per sample-grads tile
 
-int groups_bwd(const sigb_plan* p) { return (int)((p->jit.host.bwd_tasks.size() + kWarps - 1) / kWarps); }
+int groups_bwd(const sigb_plan* p, int dtype) {
+  const int w = cfg_of(p, dtype, true).warps;
+  return (int)((p->jit.host.bwd_tasks.size() + w - 1) / w);
+}
+
+int64_t pad32(int64_t n) { return (n + 31) / 32 * 32; }
 
 int64_t bwd_chunk(const sigb_plan* p, int dtype, int64_t B, int64_t L) {
-  const size_t per_path = (dtype == SIGB_F32 ? 4 : 8) * (size_t)groups_bwd(p) * (size_t)(L - 1) * p->d;
+  const size_t per_path = (dtype == SIGB_F32 ? 4 : 8) * (size_t)groups_bwd(p, dtype) * (size_t)(L - 1) * p->d;
   int64_t c = per_path ? (int64_t)(kPartialBudget / per_path) : B;
-  c = std::max<int64_t>(32, c - c % 32);
+  c = std::min<int64_t>(std::max<int64_t>(32, c - c % 32), int64_t(1) << 20);
   return std::min<int64_t>(c, B);
 }
 
+// dX[b][t] = inc(t-1) - inc(t), inc(j)[z] = sum_g partial[g][j][z][b]: a CTA
+// sums a tile of 32 paths x (kTT+1) increments (16-byte path-contiguous loads,
+// groups unrolled for memory parallelism), then writes the tile's samples row
+// by row (each path's kTT*d samples are contiguous in dX).
 template <typename T>
-__global__ void jit_sample_grads(const T* __restrict__ partial, int64_t Bc, int64_t P, int64_t M, int64_t d,
-                                 int64_t b0, T* __restrict__ dX, T* __restrict__ dinc) {
+__global__ void __launch_bounds__(256) jit_sample_grads(const T* __restrict__ partial, int64_t Bp, int64_t Bc, int P,
+                                                        int64_t M, int d, int64_t b0, T* __restrict__ dX,
+                                                        T* __restrict__ dinc) {
+  constexpr int V = 16 / sizeof(T);  // paths per 16-byte load
+  struct __align__(16) Vec { T v[V]; };
+  extern __shared__ __align__(16) unsigned char sg_raw[];
+  T* inc = reinterpret_cast<T*>(sg_raw);  // [kTT + 1][d][33]
   const int64_t L = M + 1;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= Bc * L * d) return;
-  const int64_t z = i % d, t = (i / d) % L, bl = i / (d * L);
-  auto inc = [&](int64_t j) {
-    T s = T(0);
-    for (int64_t q = 0; q < P; ++q) s += partial[((bl * P + q) * M + j) * d + z];
-    return s;
-  };
-  T v = T(0);
-  if (t >= 1) v += inc(t - 1);
-  if (t < M) {
-    const T it = inc(t);
-    v -= it;
-    if (dinc) dinc[((b0 + bl) * M + t) * d + z] = it;
+  const int64_t pb = (int64_t)blockIdx.y * 32, t0 = (int64_t)blockIdx.x * kTT;
+  const int64_t gs = M * d * Bp;
+  const int nq = (kTT + 1) * d * (32 / V);
+  for (int i = threadIdx.x; i < nq; i += blockDim.x) {
+    const int q = i % (32 / V), r = i / (32 / V);
+    const int jj = r / d, z = r - jj * d;
+    const int64_t j = t0 - 1 + jj;
+    Vec acc;
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc.v[k] = T(0);
+    if (j >= 0 && j < M) {
+      const T* src = partial + (j * d + z) * Bp + pb + q * V;
+      int g = 0;
+      for (; g + 4 <= P; g += 4) {
+        const Vec a = *reinterpret_cast<const Vec*>(src + (g + 0) * gs);
+        const Vec b = *reinterpret_cast<const Vec*>(src + (g + 1) * gs);
+        const Vec c = *reinterpret_cast<const Vec*>(src + (g + 2) * gs);
+        const Vec e = *reinterpret_cast<const Vec*>(src + (g + 3) * gs);
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc.v[k] += a.v[k] + b.v[k] + c.v[k] + e.v[k];
+      }
+      for (; g < P; ++g) {
+        const Vec a = *reinterpret_cast<const Vec*>(src + g * gs);
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc.v[k] += a.v[k];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < V; ++k) inc[r * 33 + q * V + k] = acc.v[k];
   }
-  dX[((b0 + bl) * L + t) * d + z] = v;
+  __syncthreads();
+  const int row = kTT * d;
+  for (int i = threadIdx.x; i < 32 * row; i += blockDim.x) {
+    const int p = i / row, e = i - p * row, tt = e / d, z = e - tt * d;
+    const int64_t b = pb + p, t = t0 + tt;
+    if (b >= Bc || t >= L) continue;
+    const T hi = inc[(tt * d + z) * 33 + p], lo = inc[((tt + 1) * d + z) * 33 + p];
+    dX[((b0 + b) * L + t) * d + z] = hi - lo;
+    if (dinc && t < M) dinc[((b0 + b) * M + t) * d + z] = lo;
+  }
 }
 }  // namespace
 
 size_t backward_workspace(const sigb_plan* p, int dtype, int64_t B, int64_t L) {
-  return (dtype == SIGB_F32 ? 4 : 8) * (size_t)bwd_chunk(p, dtype, B, L) * groups_bwd(p) * (size_t)(L - 1) * p->d;
+  return (dtype == SIGB_F32 ? 4 : 8) * (size_t)pad32(bwd_chunk(p, dtype, B, L)) * groups_bwd(p, dtype) *
+         (size_t)(L - 1) * p->d;
 }
 
 int backward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, const void* S, int64_t s_ld,
@@ -675,38 +878,53 @@ int backward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L,
   int rc = ensure(const_cast<sigb_plan*>(p), dtype, true);
   if (rc) return rc;
   const int di = dtype == SIGB_F32 ? 0 : 1;
-  const int groups = groups_bwd(p);
+  const Cfg& c = cfg_of(p, dtype, true);
+  const int groups = groups_bwd(p, dtype);
   const int64_t M = L - 1, d = p->d;
   const int64_t chunk = bwd_chunk(p, dtype, B, L);
   const size_t es = dtype == SIGB_F32 ? 4 : 8;
-  if (!work || work_bytes < es * (size_t)chunk * groups * M * d) return fail(SIGB_ERR_DOMAIN, "backward workspace too small");
+  if (!work || work_bytes < es * (size_t)pad32(chunk) * groups * M * d)
+    return fail(SIGB_ERR_DOMAIN, "backward workspace too small");
+  if ((uintptr_t)work % 16) return fail(SIGB_ERR_DOMAIN, "backward workspace must be 16-byte aligned");
+  static bool attr[2] = {false, false};  // sample-grads tiles above 48 KB (fp64, large d)
+  if (!attr[di]) {
+    const int mx = (int)(es * (kTT + 1) * 32 * 33);
+    SIGB_CUDA_TRY(di == 0 ? cudaFuncSetAttribute((const void*)jit_sample_grads<float>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, mx)
+                          : cudaFuncSetAttribute((const void*)jit_sample_grads<double>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    attr[di] = true;
+  }
   for (int64_t b0 = 0; b0 < B; b0 += chunk) {
     const int64_t Bc = std::min(chunk, B - b0);
     const char* Xc = (const char*)X + es * (size_t)b0 * L * d;
     const char* Sc = (const char*)S + es * (size_t)b0 * s_ld;
     const char* gc = (const char*)g + es * (size_t)b0 * g_ld;
-    long long Bl = Bc, Ll = L, sl = s_ld, s0 = s_col0, gl = g_ld, g0 = g_col0;
+    long long Bl = Bc, Ll = L, sl = s_ld, s0 = s_col0, gl = g_ld, g0 = g_col0, Bp = pad32(Bc);
     void* Xv = (void*)Xc;
     void* Sv = (void*)Sc;
     void* gv = (void*)gc;
-    int grp = groups, nblocks = (int)((Bc + 31) / 32);
+    int grp = groups, nblocks = (int)((Bc + 31) / 32), bulk = bulk_ok(Xc, dtype, d);
     int* ctr = counters(p, groups, stream);
     if (!ctr) return fail(SIGB_ERR_CUDA, "work counters for the word-set kernel");
-    void* args[] = {&Xv, &Bl, &Ll, &Sv, &sl, &s0, &gv, &gl, &g0, &work, &nblocks, &grp, &ctr};
-    const size_t smem = smem_bytes(dtype, (int)d, true);
+    void* args[] = {&Xv, &Bl, &Ll, &Sv, &sl, &s0, &gv, &gl, &g0, &work, &Bp, &nblocks, &grp, &ctr, &bulk};
+    const size_t smem = smem_bytes(dtype, (int)d, c, true);
     const void* kern = (const void*)p->jit.kern[di][1];
     count_launch(2);
     timing_begin(1, stream);
-    SIGB_CUDA_TRY(cudaLaunchKernel(kern, dim3(persistent_grid(kern, smem, (int64_t)groups * nblocks)),
-                                   dim3(32 * kWarps), args, smem, stream));
+    const int threads = 32 * c.warps * c.pb;
+    SIGB_CUDA_TRY(cudaLaunchKernel(
+        kern, dim3(persistent_grid(kern, threads, smem, ((int64_t)groups * nblocks + c.pb - 1) / c.pb)), dim3(threads),
+        args, smem, stream));
     timing_end(1, stream);
-    const int64_t n = Bc * L * d;
+    const dim3 sgrid((unsigned)((L + kTT - 1) / kTT), (unsigned)((Bc + 31) / 32));
+    const size_t ssm = es * (size_t)(kTT + 1) * d * 33;
     if (dtype == SIGB_F32)
-      jit_sample_grads<float><<<(unsigned)((n + 255) / 256), 256, 0, stream>>>((const float*)work, Bc, groups, M, d, b0,
-                                                                             (float*)dX, (float*)dinc);
+      jit_sample_grads<float><<<sgrid, 256, ssm, stream>>>((const float*)work, Bp, Bc, groups, M, (int)d, b0,
+                                                           (float*)dX, (float*)dinc);
     else
-      jit_sample_grads<double><<<(unsigned)((n + 255) / 256), 256, 0, stream>>>((const double*)work, Bc, groups, M, d,
-                                                                              b0, (double*)dX, (double*)dinc);
+      jit_sample_grads<double><<<sgrid, 256, ssm, stream>>>((const double*)work, Bp, Bc, groups, M, (int)d, b0,
+                                                            (double*)dX, (double*)dinc);
     SIGB_CUDA_TRY(cudaGetLastError());
   }
   return SIGB_OK;
