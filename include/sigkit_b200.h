@@ -173,6 +173,38 @@ int sigb_backward(const sigb_plan* plan, int dtype, const void* d_X, int64_t B, 
                   int64_t g_ld, int64_t g_col0, int64_t ckpt_stride, void* d_work, size_t work_bytes,
                   void* d_dX, void* d_dinc, void* stream);
 
+/*
+ * Log-signature polynomial (the consumers of signature_forward that
+ * logsig.py routes through the hot path).  Replaces the numpy loops of
+ * logsignature_forward (logsig.py:165-173) and logsignature_backward
+ * (logsig.py:208-222) over the host-built term table of _lyndon_projection
+ * (logsig.py:79-127): Lyndon word i has terms [term_off[i], term_off[i+1]);
+ * term t is coef[t] * prod_k sig[cols[t*F + k]] over its factor columns
+ * (F = max_factors, -1 padded), coef = (-1)^(k+1)/k for k factors.
+ *   forward:  out[b*out_ld + i] = sum_t coef[t] prod_k sig[b*sig_ld + cols[t][k]]
+ *   backward: up[b*up_ld + c] = sum over entries e of column c, e = (t << 8) | k,
+ *             of g[b*g_ld + term_word[t]] * coef[t] * prod_{k' != k} sig[..cols[t][k']]
+ *             (the column -> (term, factor) index replaces the reference's
+ *             scatter-add, so the sum runs in a fixed order).
+ */
+int sigb_logsig_forward(int dtype, const void* d_sig, int64_t B, int64_t sig_ld, const int64_t* d_term_off,
+                        const int32_t* d_cols, const double* d_coef, int64_t n_out, int max_factors, void* d_out,
+                        int64_t out_ld, void* stream);
+int sigb_logsig_backward(int dtype, const void* d_sig, int64_t B, int64_t sig_ld, const void* d_g, int64_t g_ld,
+                         const int64_t* d_col_off, const int64_t* d_entries, const int64_t* d_term_word,
+                         const int32_t* d_cols, const double* d_coef, int max_factors, int64_t ncols, void* d_up,
+                         int64_t up_ld, void* stream);
+/*
+ * Graded product of dense truncated tensors in the epsilon-first layout
+ * (width sum_{n<=N} d^n, row b at b*width): replaces _tensor_mul_full
+ * (sigcore.py:297-311), the kernel of chen_concat (sigcore.py:321-334),
+ * signature_inverse (sigcore.py:337-352), tensor_log and tensor_exp
+ * (logsig.py:42-72):  out = scale * (x (x) y), then out[:, 0] += add0.
+ * d_out must not alias d_x or d_y.
+ */
+int sigb_tensor_mul(int dtype, const void* d_x, const void* d_y, int64_t B, int64_t d, int N, double scale,
+                    double add0, void* d_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

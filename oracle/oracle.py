@@ -220,6 +220,75 @@ def dense_columns(codes, lengths, d, dense_values):
     return dense_values[:, cols]
 
 
+# -- dense truncated tensor algebra (sigcore.py:297-352, logsig.py:42-72) ----------------
+# Flat rows hold levels 1..N in canonical order (no epsilon column); the level
+# lists below carry the epsilon coefficient as level 0.
+
+
+def _levels(row, d, N, eps):
+    out, off = [np.array(float(eps))], 0
+    for n in range(1, N + 1):
+        out.append(np.asarray(row[off:off + d**n], dtype=np.float64).reshape((d,) * n))
+        off += d**n
+    return out
+
+
+def _flat(levels, N):
+    return np.concatenate([levels[n].reshape(-1) for n in range(1, N + 1)])
+
+
+def dense_product(a, b, d, N):
+    """Chen product of two flat signature batches (chen_concat, sigcore.py:321-334)."""
+    return np.stack([_flat(_dense_mul(_levels(x, d, N, 1.0), _levels(y, d, N, 1.0), N), N) for x, y in zip(a, b)])
+
+
+def dense_inverse(a, d, N):
+    """Group inverse sum_k (-x)^k (signature_inverse, sigcore.py:337-352)."""
+    rows = []
+    for r in a:
+        x = _levels(r, d, N, 0.0)
+        term, acc = _levels(np.zeros_like(r), d, N, 1.0), _levels(np.zeros_like(r), d, N, 1.0)
+        for _ in range(N):
+            term = [-t for t in _dense_mul(x, term, N)]
+            acc = [u + v for u, v in zip(acc, term)]
+        rows.append(_flat(acc, N))
+    return np.stack(rows)
+
+
+def dense_log(a, d, N):
+    """log(1 + x) = sum_k (-1)^(k+1) x^k / k of flat signature rows (tensor_log, logsig.py:42-56)."""
+    rows = []
+    for r in a:
+        x = _levels(r, d, N, 0.0)
+        power, acc = x, [np.zeros_like(t) for t in x]
+        for k in range(1, N + 1):
+            acc = [u + (1.0 if k % 2 else -1.0) / k * v for u, v in zip(acc, power)]
+            power = _dense_mul(power, x, N)
+        rows.append(_flat(acc, N))
+    return np.stack(rows)
+
+
+def dense_exp(a, d, N):
+    """exp(x) = sum_k x^k / k! of flat Lie-series rows (tensor_exp, logsig.py:59-72)."""
+    rows = []
+    for r in a:
+        x = _levels(r, d, N, 0.0)
+        power, acc, fact = x, [np.zeros_like(t) for t in x], 1.0
+        for k in range(1, N + 1):
+            fact *= k
+            acc = [u + v / fact for u, v in zip(acc, power)]
+            power = _dense_mul(power, x, N)
+        rows.append(_flat(acc, N))
+    return np.stack(rows)
+
+
+def lyndon_logsig(X, d, N, lyndon_codes, lyndon_lengths):
+    """Log-signature at Lyndon words = tensor log of the dense signature restricted to them
+    (the identity the reference tests, test_logsig.py:75-87)."""
+    full = dense_log(dense_signature(X, d, N), d, N)
+    return dense_columns(lyndon_codes, lyndon_lengths, d, full)
+
+
 def finite_difference_grad(X, codes, lengths, d, upstream, h=1e-5):
     X = np.asarray(X, dtype=np.float64)
     up = np.asarray(upstream, dtype=np.float64)

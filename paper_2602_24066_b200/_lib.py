@@ -53,6 +53,9 @@ SIGNATURES = {
     "sigb_backward_workspace_size": (_C, [_P, _C, _I, _I, _I, ctypes.POINTER(ctypes.c_size_t)]),
     "sigb_backward": (_C, [_P, _C, _P, _I, _I, _P, _I, _I, _C, _P, _I, _I, _I, _P, ctypes.c_size_t,
                            _P, _P, _P]),
+    "sigb_logsig_forward": (_C, [_C, _P, _I, _I, _P, _P, _P, _I, _C, _P, _I, _P]),
+    "sigb_logsig_backward": (_C, [_C, _P, _I, _I, _P, _I, _P, _P, _P, _P, _P, _C, _I, _P, _I, _P]),
+    "sigb_tensor_mul": (_C, [_C, _P, _P, _I, _I, _C, ctypes.c_double, ctypes.c_double, _P, _P]),
 }
 
 _lib = None
