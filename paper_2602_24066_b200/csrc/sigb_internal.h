@@ -118,6 +118,7 @@ struct Task {
 // (register budget), T-node cap per task.
 struct Cfg {
   int warps = 4, ch = 8, minb = 4, pb = 1;
+  int lock = 0;  // slots claim together and share the CTA barrier (lockstep)
   int64_t cap = 96;
 };
 }  // namespace jit

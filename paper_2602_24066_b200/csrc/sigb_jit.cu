@@ -66,12 +66,14 @@ Cfg default_cfg(int dtype, int d, bool backward) {
     c.minb = env_int("SIGB_JIT_FMINB", 1);
     c.cap = env_int("SIGB_JIT_FCAP", 96);
     c.pb = env_int("SIGB_JIT_FPB", 3);
+    c.lock = env_int("SIGB_JIT_FLOCK", 0);
   } else {
     c.warps = env_int("SIGB_JIT_BWARPS", 4);
     c.ch = env_int("SIGB_JIT_BCH", 8);
     c.minb = env_int("SIGB_JIT_BMINB", 1);
     c.cap = env_int("SIGB_JIT_BCAP", 96);
     c.pb = env_int("SIGB_JIT_BPB", 2);
+    c.lock = env_int("SIGB_JIT_BLOCK", 1);
   }
   c.warps = std::min(std::max(c.warps, 1), 16);
   c.ch = std::min(std::max(c.ch, 1), 64);
@@ -283,7 +285,7 @@ std::string common_head(int dtype, int d, const Cfg& c) {
   const int vw = vec_width(dtype, d);
   o << "typedef " << tname(dtype) << " R;\n";
   o << "#define D " << d << "\n#define CH " << c.ch << "\n#define WARPS " << c.warps << "\n#define NT (32 * WARPS)\n";
-  o << "#define PB " << c.pb << "\n";
+  o << "#define PB " << c.pb << "\n#define LOCK " << c.lock << "\n";
   o << "#define MINB " << c.minb << "\n#define VW " << vw << "\n#define PITCH " << pitch(dtype, d, c.ch) << "\n";
   o << R"(
 struct __align__(VW * sizeof(R)) RV { R v[VW]; };
@@ -305,8 +307,16 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned phase)
 }
 __device__ __forceinline__ int stid() { return (int)threadIdx.x % (32 * WARPS); }  // thread index in the slot
 __device__ __forceinline__ int slot_id() { return (int)(threadIdx.x >> 5) / WARPS; }
+// LOCK: the slots of a CTA claim their path blocks together and share the
+// CTA barrier, so the warps of one task on an SM scheduler stay in lockstep
+// (one instruction fetch serves both); otherwise each slot has its own
+// named barrier and runs free.
 __device__ __forceinline__ void slot_sync() {
+#if LOCK
+  __syncthreads();
+#else
   asm volatile("bar.sync %0, %1;" ::"r"(1 + slot_id()), "r"(32 * WARPS) : "memory");
+#endif
 }
 __device__ __forceinline__ void cp_async(R* dst, const R* src) {
   if (sizeof(R) == 4) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(su32(dst)), "l"(src) : "memory");
@@ -318,7 +328,7 @@ __device__ __forceinline__ void cp_async(R* dst, const R* src) {
 __device__ __forceinline__ void issue(const R* __restrict__ X, long long B, long long L, long long b0, long long j0,
                                       int cs, R* __restrict__ Xs, unsigned long long* mbar, int bulk) {
   const int rows = (cs + 1) * D;
-  const long long nl = B - b0 < 32 ? B - b0 : 32;
+  const long long nl = B - b0 < 32 ? (B > b0 ? B - b0 : 0) : 32;
   if (bulk) {
     if (stid() < 32) {
       const int p = stid();
@@ -415,12 +425,22 @@ extern "C" __global__ void __launch_bounds__(NT * PB, MINB) sigjit_fwd(const R* 
   for (int pass = 0; pass < groups; ++pass) {
    const int g = (g0 + pass) % groups;
    for (;;) {
+#if LOCK
+    if (threadIdx.x == 0) works[0] = atomicAdd(counters + g, PB);
+    __syncthreads();
+    const int pbase = works[0];
+    __syncthreads();
+    if (pbase >= nblocks) break;
+    const int pb = pbase + slot_id();
+    const int task = pb < nblocks ? g * WARPS + (threadIdx.x >> 5) % WARPS : 0x7fffffff;  // idle slot
+#else
     if (stid() == 0) works[slot_id()] = atomicAdd(counters + g, 1);
     slot_sync();
     const int pb = works[slot_id()];
     slot_sync();
     if (pb >= nblocks) break;
     const int task = g * WARPS + (threadIdx.x >> 5) % WARPS;
+#endif
     const long long b0 = (long long)pb * 32, b = b0 + lane;
     const bool live = b < B;
     R* orow = out && live ? out + b * out_ld + out_col0 : nullptr;
@@ -466,6 +486,7 @@ std::string gen_backward(const Trie& t, const std::vector<Task>& tasks, int dtyp
 // into partial[g][j0+s][z][path] (path pitch Bp), fixed warp order.
 __device__ __forceinline__ void reduce(const R* __restrict__ Gb, long long j0, int cs, R* __restrict__ partial,
                                        long long Bp, long long M, int g, long long b0) {
+  if (b0 >= Bp) return;  // idle slot (LOCK): no paths
   for (int i = stid(); i < cs * D * (32 / VW); i += NT) {
     const int q = i % (32 / VW), sz = i / (32 / VW);
     RV acc = *reinterpret_cast<const RV*>(Gb + sz * 32 + q * VW);
@@ -530,12 +551,22 @@ extern "C" __global__ void __launch_bounds__(NT * PB, MINB) sigjit_bwd(const R* 
    slot_sync();
    for (int i = stid(); i < WARPS * CH * D * 32; i += NT) Gb[i] = R(0);  // new tasks, new letters
    for (;;) {
+#if LOCK
+    if (threadIdx.x == 0) works[0] = atomicAdd(counters + g, PB);
+    __syncthreads();
+    const int pbase = works[0];
+    __syncthreads();
+    if (pbase >= nblocks) break;
+    const int pb = pbase + slot_id();
+    const int task = pb < nblocks ? g * WARPS + (threadIdx.x >> 5) % WARPS : 0x7fffffff;  // idle slot
+#else
     if (stid() == 0) works[slot_id()] = atomicAdd(counters + g, 1);
     slot_sync();
     const int pb = works[slot_id()];
     slot_sync();
     if (pb >= nblocks) break;
     const int task = g * WARPS + (threadIdx.x >> 5) % WARPS;
+#endif
     const long long b0 = (long long)pb * 32, b = b0 + lane;
     const bool live = b < B;
     const R* srow = Sin + (live ? b : 0) * s_ld + s_col0;
