@@ -168,10 +168,6 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(loaded)}
 
 
-def s_el_bench(dt) -> int:
-    return 8 if dt == torch.float64 else 4
-
-
 def cpu_threads() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -352,7 +348,7 @@ def run_ours(args) -> None:
     l2_note = ("flushed: 256 MB written between timed steps outside the CUDA-event brackets "
                "(X+S+g %.3f GB per rank < 2 x L2)" % (step_bytes / 1e9) if flush is not None else
                "no flush: every pass streams inputs larger than L2 (X %.2f GB, S %.2f GB per rank)"
-               % (B * L * d * s_el_bench(tdt) / 1e9, B * W * s_el_bench(tdt) / 1e9))
+               % (B * L * d * X.element_size() / 1e9, B * W * X.element_size() / 1e9))
 
     clocks = ClockSampler(enabled=(local == 0))
     _lib.timing_enable(True)
