@@ -259,8 +259,21 @@ __device__ __forceinline__ void chen_step(State<T, D, N, G>& st, const StepIncr<
   for (int g = 0; g < G; ++g) {
     if constexpr (Leaves) {
       const T tm = fma(in.dy[g] * inv<T, 2>(), tN, st.mid[g]);  // T(u_g, N)
+      if constexpr (sizeof(T) == 4 && D % 2 == 0) {
+        // packed f32x2 FMAs: half the issue slots for the leaf level (the FMA
+        // pipe still does one lane-FMA per cycle, see tools/ubench_fma.cu)
+        const float2 tm2 = make_float2(tm, tm);
 #pragma unroll
-      for (int z = 0; z < D; ++z) st.leaf[g][z] = fma(in.dz[z], tm, st.leaf[g][z]);
+        for (int z = 0; z < D; z += 2) {
+          const float2 r = __ffma2_rn(make_float2(in.dz[z], in.dz[z + 1]), tm2,
+                                      make_float2(st.leaf[g][z], st.leaf[g][z + 1]));
+          st.leaf[g][z] = r.x;
+          st.leaf[g][z + 1] = r.y;
+        }
+      } else {
+#pragma unroll
+        for (int z = 0; z < D; ++z) st.leaf[g][z] = fma(in.dz[z], tm, st.leaf[g][z]);
+      }
     }
     st.mid[g] = fma(in.dy[g], tN1, st.mid[g]);
   }
@@ -483,13 +496,29 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
       for (int g = 0; g < G; ++g) {
         const T tm = fma(in.dy[g] * inv<T, 2>(), tN, st.mid[g]);  // T(u_g, N)
         T tb0 = T(0), tb1 = T(0);
+        if constexpr (sizeof(T) == 4 && D % 2 == 0) {
+          // packed f32x2: even/odd letters in the two halves (as the scalar split)
+          float2 tb2 = make_float2(0.f, 0.f);
+          const float2 tm2 = make_float2(tm, tm);
 #pragma unroll
-        for (int z = 0; z < D; z += 2) {
-          tb0 = fma(in.dz[z], lam.leaf[g][z], tb0);
-          gl[z] = fma(lam.leaf[g][z], tm, gl[z]);
-          if (z + 1 < D) {
-            tb1 = fma(in.dz[z + 1], lam.leaf[g][z + 1], tb1);
-            gl[z + 1] = fma(lam.leaf[g][z + 1], tm, gl[z + 1]);
+          for (int z = 0; z < D; z += 2) {
+            const float2 lz = make_float2(lam.leaf[g][z], lam.leaf[g][z + 1]);
+            tb2 = __ffma2_rn(make_float2(in.dz[z], in.dz[z + 1]), lz, tb2);
+            const float2 r = __ffma2_rn(lz, tm2, make_float2(gl[z], gl[z + 1]));
+            gl[z] = r.x;
+            gl[z + 1] = r.y;
+          }
+          tb0 = tb2.x;
+          tb1 = tb2.y;
+        } else {
+#pragma unroll
+          for (int z = 0; z < D; z += 2) {
+            tb0 = fma(in.dz[z], lam.leaf[g][z], tb0);
+            gl[z] = fma(lam.leaf[g][z], tm, gl[z]);
+            if (z + 1 < D) {
+              tb1 = fma(in.dz[z + 1], lam.leaf[g][z + 1], tb1);
+              gl[z + 1] = fma(lam.leaf[g][z + 1], tm, gl[z + 1]);
+            }
           }
         }
         const T tb = tb0 + tb1;  // Tbar(u_g, N)
