@@ -119,8 +119,21 @@ __device__ __forceinline__ void chen_step(FState<T, NC, G, K>& st, const FIncr<T
   for (int g = 0; g < G; ++g) {
     if constexpr (Leaves) {
       const T tm = fma(in.dy[g] * T(0.5), tN, st.mid[g]);  // T(mid_g, NV)
+      if constexpr (sizeof(T) == 4) {
+        // packed f32x2 FMAs for pairs of leaves (half the issue slots)
+        const float2 tm2 = make_float2(tm, tm);
 #pragma unroll
-      for (int k = 0; k < K; ++k) st.leaf[g][k] = fma(in.dz[k], tm, st.leaf[g][k]);
+        for (int k = 0; k + 1 < K; k += 2) {
+          const float2 r = __ffma2_rn(make_float2(in.dz[k], in.dz[k + 1]), tm2,
+                                      make_float2(st.leaf[g][k], st.leaf[g][k + 1]));
+          st.leaf[g][k] = r.x;
+          st.leaf[g][k + 1] = r.y;
+        }
+        if constexpr (K % 2) st.leaf[g][K - 1] = fma(in.dz[K - 1], tm, st.leaf[g][K - 1]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) st.leaf[g][k] = fma(in.dz[k], tm, st.leaf[g][k]);
+      }
     }
     st.mid[g] = fma(in.dy[g], tN1, st.mid[g]);
   }
@@ -326,10 +339,29 @@ __global__ void __launch_bounds__(kTPB) frag_backward_kernel(FragDev fd, const T
       for (int g = 0; g < G; ++g) {
         const T tm = fma(in.dy[g] * T(0.5), tN, st.mid[g]);
         T tb = T(0);
+        if constexpr (sizeof(T) == 4 && K >= 2) {
+          // packed f32x2: leaf pairs; the adjoint dot product keeps two partial sums
+          float2 tb2 = make_float2(0.f, 0.f);
+          const float2 tm2 = make_float2(tm, tm);
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-          tb = fma(in.dz[k], lam.leaf[g][k], tb);
-          gl[k] = fma(lam.leaf[g][k], tm, gl[k]);
+          for (int k = 0; k + 1 < K; k += 2) {
+            const float2 lz = make_float2(lam.leaf[g][k], lam.leaf[g][k + 1]);
+            tb2 = __ffma2_rn(make_float2(in.dz[k], in.dz[k + 1]), lz, tb2);
+            const float2 r = __ffma2_rn(lz, tm2, make_float2(gl[k], gl[k + 1]));
+            gl[k] = r.x;
+            gl[k + 1] = r.y;
+          }
+          if constexpr (K % 2) {
+            tb2.x = fma(in.dz[K - 1], lam.leaf[g][K - 1], tb2.x);
+            gl[K - 1] = fma(lam.leaf[g][K - 1], tm, gl[K - 1]);
+          }
+          tb = tb2.x + tb2.y;
+        } else {
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            tb = fma(in.dz[k], lam.leaf[g][k], tb);
+            gl[k] = fma(lam.leaf[g][k], tm, gl[k]);
+          }
         }
         const T lm = lam.mid[g];
         tbp1 = fma(in.dy[g], lm, tbp1);
