@@ -123,6 +123,11 @@ int sigb_fragment_plan_info(const uint64_t* codes, const int64_t* lengths, int64
  * length to *len.  SIGB_ERR_UNSUPPORTED when the set is too large. */
 int sigb_jit_source(const uint64_t* codes, const int64_t* lengths, int64_t W, int64_t d, int dtype, int backward,
                     char* buf, size_t cap, size_t* len);
+/* Host-only: generate and NVRTC-compile the set's kernel for sm_100a into the
+ * cubin cache (jit_cache/ next to the library, or $SIGB_JIT_CACHE), so a
+ * device process loads it instead of compiling on first use.  The build runs
+ * it for the shipped word sets (config 3). */
+int sigb_jit_precompile(const uint64_t* codes, const int64_t* lengths, int64_t W, int64_t d, int dtype, int backward);
 
 /*
  * Forward signature.  Replaces forward_kernel (_kernels.py:40-58) together

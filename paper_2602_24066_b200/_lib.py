@@ -48,6 +48,7 @@ SIGNATURES = {
     "sigb_plan_kernel_kind": (_C, [_P]),
     "sigb_fragment_plan_info": (_C, [_P, _P, _I, _I, _P]),
     "sigb_jit_source": (_C, [_P, _P, _I, _I, _C, _C, _P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
+    "sigb_jit_precompile": (_C, [_P, _P, _I, _I, _C, _C]),
     "sigb_forward": (_C, [_P, _C, _P, _I, _I, _P, _I, _I, _C, _P, _P]),
     "sigb_windows": (_C, [_P, _C, _P, _I, _I, _P, _I, _P, _P]),
     "sigb_backward_workspace_size": (_C, [_P, _C, _I, _I, _I, ctypes.POINTER(ctypes.c_size_t)]),
@@ -121,6 +122,15 @@ def fragment_plan_info(codes, lengths, d: int) -> dict:
     check(lib().sigb_fragment_plan_info(c.ctypes.data, n.ctypes.data, int(n.size), int(d), info.ctypes.data))
     keys = ("NC", "G", "K", "fragments", "ctas_per_path", "closure", "cost", "instantiated")
     return dict(zip(keys, (int(v) for v in info)))
+
+
+def jit_precompile(codes, lengths, d: int, dtype: int = SIGB_F32, backward: bool = False) -> None:
+    """Host-only: compile a small word set's generated kernel into the cubin cache (sigb_jit_precompile)."""
+    import numpy as np
+
+    c = np.ascontiguousarray(codes, dtype=np.uint64)
+    n = np.ascontiguousarray(lengths, dtype=np.int64)
+    check(lib().sigb_jit_precompile(c.ctypes.data, n.ctypes.data, int(n.size), int(d), int(dtype), int(backward)))
 
 
 def jit_source(codes, lengths, d: int, dtype: int = SIGB_F32, backward: bool = False) -> str:

@@ -53,6 +53,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
+def precompile_shipped() -> None:
+    """NVRTC-compile the generated kernels of the shipped small word set (config 3,
+    fp32 forward + backward) into jit_cache/ next to the library, host-only, so a
+    device process (smoke, tests, bench) loads cubins instead of compiling."""
+    import json
+
+    import numpy as np
+
+    from . import _lib
+    from .wordset import build_custom
+
+    words = os.path.join(os.path.dirname(HERE), "tests", "golden", "c3_words.json")
+    if not os.path.exists(words):
+        return
+    with open(words) as f:
+        ws = build_custom([tuple(w) for w in json.load(f)["words"]], 16)
+    for backward in (False, True):
+        _lib.jit_precompile(np.asarray(ws.codes), np.asarray(ws.lengths), ws.d, _lib.SIGB_F32, backward)
+
+
 def build_ubench(force: bool = False) -> str:
     """tools/ubench_fma: the FFMA/DFMA pipe microbenchmark bench.py uses for the roofline peak."""
     root = os.path.dirname(HERE)

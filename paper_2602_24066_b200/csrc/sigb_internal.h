@@ -143,6 +143,7 @@ bool eligible(const Trie& t);
 void make_plan(const Trie& t, JitHost& h);
 std::string source(const Trie& t, const JitHost& h, int dtype, bool backward);
 int ensure(sigb_plan* p, int dtype, bool backward);  // compile / load; SIGB_OK or error
+int precompile(const Trie& t, int dtype, bool backward);  // host-only: fill the cubin cache
 int forward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, void* out, int64_t out_ld,
             int64_t out_col0, int include_empty, void* state, cudaStream_t stream);
 size_t backward_workspace(const sigb_plan* p, int dtype, int64_t B, int64_t L);

@@ -25,6 +25,7 @@
 // fixed order once per chunk, behind the barrier the chunk staging needs
 // anyway.  Partials [group][step][letter][path] are summed over groups and
 // telescoped into dL/dX by jit_sample_grads.
+#include <dlfcn.h>
 #include <nvrtc.h>
 
 #include <algorithm>
@@ -679,10 +680,22 @@ size_t smem_bytes(int dtype, int d, const Cfg& c, bool backward) {
 
 namespace {
 
-std::string cache_dir() {
-  if (const char* e = getenv("SIGB_JIT_CACHE")) return e;
+// Cubin cache directories, searched in order: $SIGB_JIT_CACHE alone if set,
+// else jit_cache/ next to libsigkit_b200.so (filled by the build for the
+// shipped word sets, travels with the tree) and ~/.cache/sigkit_b200/jit.
+// New cubins go to the first writable one.
+std::vector<std::string> cache_dirs() {
+  if (const char* e = getenv("SIGB_JIT_CACHE")) return {e};
+  std::vector<std::string> dirs;
+  Dl_info info;
+  if (dladdr((void*)&cache_dirs, &info) && info.dli_fname) {
+    std::string so = info.dli_fname;
+    const size_t k = so.find_last_of('/');
+    dirs.push_back((k == std::string::npos ? std::string(".") : so.substr(0, k)) + "/jit_cache");
+  }
   const char* home = getenv("HOME");
-  return std::string(home ? home : "/tmp") + "/.cache/sigkit_b200/jit";
+  dirs.push_back(std::string(home ? home : "/tmp") + "/.cache/sigkit_b200/jit");
+  return dirs;
 }
 
 void mkdirs(const std::string& path) {
@@ -696,9 +709,9 @@ void mkdirs(const std::string& path) {
 // NVRTC -> cubin for sm_100a (cached on disk by a hash of the source).
 int compile(const std::string& src, std::string& cubin) {
   const std::string key = std::to_string(std::hash<std::string>{}(src)) + "_" + std::to_string(src.size());
-  const std::string dir = cache_dir(), path = dir + "/" + key + ".cubin";
-  {
-    std::ifstream in(path, std::ios::binary);
+  const std::vector<std::string> dirs = cache_dirs();
+  for (const std::string& dir : dirs) {
+    std::ifstream in(dir + "/" + key + ".cubin", std::ios::binary);
     if (in) {
       cubin.assign(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>());
       if (!cubin.empty()) return SIGB_OK;
@@ -722,12 +735,14 @@ int compile(const std::string& src, std::string& cubin) {
   cubin.assign(n, '\0');
   nvrtcGetCUBIN(prog, &cubin[0]);
   nvrtcDestroyProgram(&prog);
-  mkdirs(dir);
-  std::ofstream out(path + ".tmp", std::ios::binary);
-  if (out) {
+  for (const std::string& dir : dirs) {
+    mkdirs(dir);
+    const std::string path = dir + "/" + key + ".cubin";
+    std::ofstream out(path + ".tmp", std::ios::binary);
+    if (!out) continue;
     out.write(cubin.data(), (std::streamsize)cubin.size());
     out.close();
-    std::rename((path + ".tmp").c_str(), path.c_str());
+    if (out && std::rename((path + ".tmp").c_str(), path.c_str()) == 0) break;
   }
   return SIGB_OK;
 }
@@ -737,6 +752,14 @@ const Cfg& cfg_of(const sigb_plan* p, int dtype, bool backward) {
 }
 
 }  // namespace
+
+// Host-only: generate and compile a word set's kernel into the cache (no device).
+int precompile(const Trie& t, int dtype, bool backward) {
+  JitHost h;
+  make_plan(t, h);
+  std::string cubin;
+  return compile(source(t, h, dtype, backward), cubin);
+}
 
 int ensure(sigb_plan* p, int dtype, bool backward) {
   JitPlan& J = p->jit;

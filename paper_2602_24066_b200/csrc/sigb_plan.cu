@@ -181,6 +181,16 @@ extern "C" int sigb_jit_source(const uint64_t* codes, const int64_t* lengths, in
   return SIGB_OK;
 }
 
+extern "C" int sigb_jit_precompile(const uint64_t* codes, const int64_t* lengths, int64_t W, int64_t d, int dtype,
+                                   int backward) {
+  if (dtype != SIGB_F32 && dtype != SIGB_F64) return fail(SIGB_ERR_SHAPE, "unsupported dtype; use float64 or float32");
+  Trie t;
+  int rc = build_trie(codes, lengths, W, d, false, nullptr, t);
+  if (rc) return rc;
+  if (!jit::eligible(t)) return fail(SIGB_ERR_UNSUPPORTED, "word set too large for generated kernels");
+  return jit::precompile(t, dtype, backward != 0);
+}
+
 extern "C" int sigb_plan_create(const uint64_t* codes, const int64_t* lengths, int64_t W, int64_t d,
                                 sigb_plan** plan_out, void* stream_) {
   if (!plan_out) return fail(SIGB_ERR_DOMAIN, "plan output pointer is NULL");
