@@ -50,7 +50,12 @@ STALL = re.compile(r"smsp__average_warps_issue_stalled_(\w+)_per_issue_active\.r
 
 
 def raw_rows(rep: str):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """Rows of `ncu -i REP --page raw --csv` (or of that CSV saved on the GPU box)."""
+    if rep.endswith(".csv"):
+        with open(rep) as f:
+            out = f.read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     return [(dict(zip(hdr, r)), dict(zip(hdr, units))) for r in rows[2:]]
