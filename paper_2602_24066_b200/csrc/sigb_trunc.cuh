@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
       if (b >= B) continue;
       T acc = T(0);
       // leaf letters: the warps / reduction groups belonging to path slot pc
-#pragma unroll 1
+#pragma unroll
       for (int w = 0; w < C::NW; ++w) {
 #pragma unroll
         for (int r = 0; r < RG::RGW; ++r) {
@@ -597,11 +597,22 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
           acc += red_leaf[w][r][s][z];
         }
       }
-      // chain terms whose letter is z, in the fixed list order
+      // chain terms whose letter is z, in the fixed list order; four independent
+      // partial sums so the list's dependent loads pipeline
       const T* rc = &red_chain[0][0][s][0][0];
       const int key = pc * D + z;
+      T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
+      int e = key_off[key];
+      const int e1 = key_off[key + 1];
 #pragma unroll 1
-      for (int e = key_off[key]; e < key_off[key + 1]; ++e) acc += rc[key_idx[e]];
+      for (; e + 4 <= e1; e += 4) {
+        a0 += rc[key_idx[e]];
+        a1 += rc[key_idx[e + 1]];
+        a2 += rc[key_idx[e + 2]];
+        a3 += rc[key_idx[e + 3]];
+      }
+      for (; e < e1; ++e) a0 += rc[key_idx[e]];
+      acc += (a0 + a1) + (a2 + a3);
       partial[(((b - b0) * C::CPP + f.cip) * M + j0 + s) * D + z] = acc;
     }
     __syncthreads();
