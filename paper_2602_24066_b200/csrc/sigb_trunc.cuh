@@ -131,6 +131,30 @@ __device__ __forceinline__ void stage_increments(const T* __restrict__ X, int64_
   __syncthreads();
 }
 
+// Backward staging, asynchronous: element cp.async of the samples of steps
+// [j0, j0+cs] into Xb (layout of stage_increments); one commit group.  The
+// backward issues chunk c-1 while chunk c computes.
+template <typename T, int D, int PPC>
+__device__ __forceinline__ void issue_samples(const T* __restrict__ X, int64_t b_first, int64_t B, int64_t L, int j0,
+                                              int cs, T* __restrict__ Xb) {
+  const int rows = cs + 1;
+  for (int i = threadIdx.x; i < PPC * rows * D; i += blockDim.x) {
+    const int pc = i / (rows * D), r = i % (rows * D);
+    const int64_t b = b_first + pc;
+    T* dst = Xb + pc * (kChunkT + 1) * D + r;
+    if (b < B) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+      if (sizeof(T) == 4)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(X + (b * L + j0) * D + r) : "memory");
+      else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(X + (b * L + j0) * D + r) : "memory");
+    } else {
+      *dst = T(0);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 // Register prefetch of the samples of the next chunk (forward): issued before
 // the current chunk's steps so the global-load latency hides behind them.
 template <typename T, int D, int PPC, int CH, int NT>
@@ -386,7 +410,8 @@ struct RedGeom {
   static constexpr size_t smem_bytes() {
     return sizeof(T) * ((size_t)C::PPC * (kChunkT + 1) * D + (size_t)C::PPC * kChunkT * D +
                         (size_t)C::NW * RGW * kChunkT * D + (size_t)C::NW * RGW * kChunkT * GPW * (C::NC > 0 ? C::NC : 1)) +
-           sizeof(int) * (NKEY + 1) + sizeof(unsigned short) * NE;
+           sizeof(int) * (NKEY + 1) + sizeof(unsigned short) * NE + 16 +
+           sizeof(T) * (size_t)C::PPC * (kChunkT + 1) * D;  // second sample buffer (async staging)
   }
 };
 
@@ -413,6 +438,8 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
   int* key_off = reinterpret_cast<int*>(Dl + C::PPC * kChunkT * D + C::NW * RG::RGW * kChunkT * D +
                                         C::NW * RG::RGW * kChunkT * RG::GPW * NCc);
   unsigned short* key_idx = reinterpret_cast<unsigned short*>(key_off + RG::NKEY + 1);
+  T* Xs2 = reinterpret_cast<T*>(
+      smem_raw + ((((size_t)(reinterpret_cast<unsigned char*>(key_idx + RG::NE) - smem_raw)) + 15) & ~size_t(15)));
   const int64_t cta = blockIdx.x + (C::CPP > 1 ? b0 * C::CPP : b0 / C::PPC);
   const Frag<D, N, G> f(cta, threadIdx.x);
   const int64_t b_first = C::CPP > 1 ? f.b : cta * C::PPC;
@@ -464,10 +491,29 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
     }
   }
   const int nchunks = (int)((M + kChunkT - 1) / kChunkT);
+  // asynchronous double-buffered staging measured faster at D = 16 (config 5,
+  // 406.8 vs 413.9 ms) and slower at D = 8 (config 2, 11.78 vs 11.00 ms)
+  constexpr bool ASYNC = D >= 16;
+  if (ASYNC && nchunks > 0)
+    issue_samples<T, D, C::PPC>(X, b_first, B, L, (nchunks - 1) * kChunkT,
+                                (int)(M - (nchunks - 1) * kChunkT), Xs);
   for (int c = nchunks - 1; c >= 0; --c) {
     const int j0 = c * kChunkT;
     const int cs = (int)(M - j0 < kChunkT ? M - j0 : kChunkT);
-    stage_increments<T, D, C::PPC>(X, b_first, B, L, j0, cs, Xs, Dl);
+    if constexpr (ASYNC) {
+      T* Xb = ((nchunks - 1 - c) & 1) ? Xs2 : Xs;
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncthreads();  // chunk c landed (every thread's copies); Dl free
+      for (int i = threadIdx.x; i < C::PPC * cs * D; i += blockDim.x) {
+        const int pc = i / (cs * D), r = i % (cs * D);
+        const T* xs = Xb + pc * (kChunkT + 1) * D;
+        Dl[pc * kChunkT * D + r] = xs[r + D] - xs[r];
+      }
+      __syncthreads();
+      if (c > 0) issue_samples<T, D, C::PPC>(X, b_first, B, L, j0 - kChunkT, kChunkT, Xb == Xs ? Xs2 : Xs);
+    } else {
+      stage_increments<T, D, C::PPC>(X, b_first, B, L, j0, cs, Xs, Dl);
+    }
     const T* rows = Dl + f.pc * kChunkT * D;
 #pragma unroll 1
     for (int s = cs - 1; s >= 0; --s) {
