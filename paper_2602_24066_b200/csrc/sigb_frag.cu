@@ -30,7 +30,7 @@ int fwd(const sigb_plan* p, const T* X, int64_t B, int64_t L, const int64_t* bou
   const int d = (int)p->d;
   const int64_t grid = B * p->frag.cpp;
   if (grid == 0) return SIGB_OK;
-  const size_t smem = sizeof(T) * ((size_t)(kChunkF + 1) * d + (size_t)kChunkF * (d + 1));
+  const size_t smem = sizeof(T) * (2 * (size_t)(kChunkF + 1) * d + (size_t)kChunkF * (d + 1));
   if (smem > 48 * 1024)
     SIGB_CUDA_TRY(cudaFuncSetAttribute(frag_forward_kernel<T, NC, G, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));

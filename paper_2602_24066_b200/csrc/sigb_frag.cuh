@@ -202,6 +202,31 @@ __device__ __forceinline__ void stage(const T* __restrict__ Xb, int d, int j0, i
   __syncthreads();
 }
 
+// Asynchronous staging: element cp.async of samples [j0, j0+cs] into Xs (one
+// commit group); diff_rows turns a landed buffer into Dl.  The kernels issue
+// chunk c+1 (forward) / c-1 (backward) while chunk c computes.
+template <typename T>
+__device__ __forceinline__ void issue_rows(const T* __restrict__ Xb, int d, int j0, int cs, T* __restrict__ Xs) {
+  const T* src = Xb + (int64_t)j0 * d;
+  for (int i = threadIdx.x; i < (cs + 1) * d; i += blockDim.x) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(Xs + i);
+    if (sizeof(T) == 4) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(src + i) : "memory");
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src + i) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <typename T>
+__device__ __forceinline__ void diff_rows(const T* __restrict__ Xs, int d, int cs, T* __restrict__ Dl) {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();  // the chunk landed for every thread; nobody reads Dl any more
+  const int rs = d + 1;
+  for (int i = threadIdx.x; i < cs * rs; i += blockDim.x) {
+    const int s = i / rs, z = i % rs;
+    Dl[i] = z < d ? Xs[(s + 1) * d + z] - Xs[s * d + z] : T(0);
+  }
+  __syncthreads();
+}
+
 template <typename T, int NC, int G, int K>
 __global__ void __launch_bounds__(kTPB) frag_forward_kernel(FragDev fd, const T* __restrict__ X, int64_t L,
                                                             const int64_t* __restrict__ bounds, int64_t nwin,
@@ -223,16 +248,20 @@ __global__ void __launch_bounds__(kTPB) frag_forward_kernel(FragDev fd, const T*
     M = bounds[2 * k + 1] - lo;
     Xb = X + ((b / nwin) * L + lo) * fd.d;
   }
-  for (int64_t j0 = 0; j0 < M; j0 += kChunkF) {
+  T* Xs2 = Dl + kChunkF * (fd.d + 1);  // second sample buffer
+  if (M > 0) issue_rows<T>(Xb, fd.d, 0, (int)(M < kChunkF ? M : kChunkF), Xs);
+  for (int64_t j0 = 0, c = 0; j0 < M; j0 += kChunkF, ++c) {
     const int cs = (int)(M - j0 < kChunkF ? M - j0 : kChunkF);
-    stage<T>(Xb, fd.d, (int)j0, cs, Xs, Dl);
+    T* Xc = (c & 1) ? Xs2 : Xs;
+    diff_rows<T>(Xc, fd.d, cs, Dl);
+    const int64_t j1 = j0 + kChunkF;
+    if (j1 < M) issue_rows<T>(Xb, fd.d, (int)j1, (int)(M - j1 < kChunkF ? M - j1 : kChunkF), (c & 1) ? Xs : Xs2);
 #pragma unroll 1
     for (int s = 0; s < cs; ++s) {
       FIncr<T, NC, G, K> in;
       gather<T, NC, G, K>(Dl + s * (fd.d + 1), lt, T(1), in);
       chen_step<T, NC, G, K>(st, in);
     }
-    __syncthreads();
   }
   T* orow = out ? out + b * out_ld + out_col0 : nullptr;
   T* srow = state ? state + b * Wc : nullptr;
@@ -260,7 +289,8 @@ __device__ __forceinline__ void load4(const double* p, double& a, double& b, dou
 
 template <int NC, int G, int K>
 __host__ __device__ constexpr size_t bwd_smem_elems(int d, int pstride) {
-  return (((size_t)(kChunkF + 1) * d + (size_t)kChunkF * (d + 1) + 3) / 4) * 4 + (size_t)kRedSteps * pstride;
+  return (((size_t)(kChunkF + 1) * d + (size_t)kChunkF * (d + 1) + 3) / 4) * 4 + (size_t)kRedSteps * pstride +
+         (size_t)(kChunkF + 1) * d;  // + second sample buffer
 }
 
 // Backward over paths [b0, b0 + gridDim.x / cpp).  partial layout:
@@ -311,10 +341,14 @@ __global__ void __launch_bounds__(kTPB) frag_backward_kernel(FragDev fd, const T
   const T* Xb = X + b * L * d;
   T* pout = partial + (bl * fd.cpp + cip) * M * d;
   const int nchunks = (int)((M + kChunkF - 1) / kChunkF);
+  T* Xs2 = buf + (size_t)kRedSteps * fd.pstride;  // second sample buffer
+  if (nchunks > 0) issue_rows<T>(Xb, d, (nchunks - 1) * kChunkF, (int)(M - (nchunks - 1) * kChunkF), Xs);
   for (int c = nchunks - 1; c >= 0; --c) {
     const int j0 = c * kChunkF;
     const int cs = (int)(M - j0 < kChunkF ? M - j0 : kChunkF);
-    stage<T>(Xb, d, j0, cs, Xs, Dl);
+    T* Xc = ((nchunks - 1 - c) & 1) ? Xs2 : Xs;
+    diff_rows<T>(Xc, d, cs, Dl);
+    if (c > 0) issue_rows<T>(Xb, d, j0 - kChunkF, kChunkF, Xc == Xs ? Xs2 : Xs);
     int nbuf = 0;  // steps parked in buf
 #pragma unroll 1
     for (int s = cs - 1; s >= 0; --s) {
