@@ -462,8 +462,29 @@ __global__ void __launch_bounds__(kTPB) frag_backward_kernel(FragDev fd, const T
           T acc = T(0);
           if (sg < kRedSteps * d && r < nbuf) {
             const T* pr = buf + (size_t)r * fd.pstride;
-            T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
-            for (int q = roff[z] + sub; q < roff[z + 1]; q += lps) {
+            // two float4 accumulators and four loads in flight per lane (the
+            // run is ~60 float4s at c4: latency, not bandwidth, bound this loop)
+            T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0), b0 = T(0), b1 = T(0), b2 = T(0), b3 = T(0);
+            const int q1 = roff[z + 1];
+            int q = roff[z] + sub;
+#pragma unroll 1
+            for (; q + 3 * lps < q1; q += 4 * lps) {
+              T v0, v1, v2, v3, w0, w1, w2, w3, x0, x1, x2, x3, y0, y1, y2, y3;
+              load4(pr + 4 * q, v0, v1, v2, v3);
+              load4(pr + 4 * (q + lps), w0, w1, w2, w3);
+              load4(pr + 4 * (q + 2 * lps), x0, x1, x2, x3);
+              load4(pr + 4 * (q + 3 * lps), y0, y1, y2, y3);
+              a0 += v0 + x0;
+              a1 += v1 + x1;
+              a2 += v2 + x2;
+              a3 += v3 + x3;
+              b0 += w0 + y0;
+              b1 += w1 + y1;
+              b2 += w2 + y2;
+              b3 += w3 + y3;
+            }
+#pragma unroll 1
+            for (; q < q1; q += lps) {
               T v0, v1, v2, v3;
               load4(pr + 4 * q, v0, v1, v2, v3);
               a0 += v0;
@@ -471,7 +492,7 @@ __global__ void __launch_bounds__(kTPB) frag_backward_kernel(FragDev fd, const T
               a2 += v2;
               a3 += v3;
             }
-            acc = (a0 + a1) + (a2 + a3);
+            acc = ((a0 + b0) + (a1 + b1)) + ((a2 + b2) + (a3 + b3));
           }
           for (int o = lps / 2; o > 0; o /= 2) acc += __shfl_xor_sync(0xffffffffu, acc, o);
           if (sg < kRedSteps * d && r < nbuf && sub == 0) {
