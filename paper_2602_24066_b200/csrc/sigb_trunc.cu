@@ -2,6 +2,8 @@
 // A plan whose closure is a full truncation (all D^n words of every length
 // 1..N) is routed here when (D, N) has an instantiation; everything else
 // runs the generic trie kernels of sigb_level.cu.
+#include <cstdlib>
+
 #include "sigb_trunc.cuh"
 
 namespace sigb {
@@ -74,16 +76,18 @@ int bwd(const T* X, int64_t B, int64_t L, const T* S, int64_t s_ld, int64_t s_co
   if (work_bytes < bwd_workspace<T, D, N, G>(B, L) || !work)
     return fail(SIGB_ERR_DOMAIN, "backward workspace too small");
   constexpr size_t smem = RG::template smem_bytes<T>();
-  SIGB_CUDA_TRY(cudaFuncSetAttribute(trunc_backward_kernel<T, D, N, G>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // experiment knob: SIGB_TRUNC_ASYNC=0/1 forces the staging mode (default: D >= 16)
+  static const int force_async = getenv("SIGB_TRUNC_ASYNC") ? atoi(getenv("SIGB_TRUNC_ASYNC")) : -1;
+  const bool async = force_async < 0 ? (D >= 16) : force_async != 0;
+  auto kern = async ? trunc_backward_kernel<T, D, N, G, true> : trunc_backward_kernel<T, D, N, G, false>;
+  SIGB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   T* partial = (T*)work;
   for (int64_t b0 = 0; b0 < B; b0 += chunk) {
     const int64_t Bc = std::min(chunk, B - b0);
     const int64_t grid = C::CPP > 1 ? Bc * C::CPP : (Bc + C::PPC - 1) / C::PPC;
     count_launch(2);
     timing_begin(1, stream);
-    trunc_backward_kernel<T, D, N, G><<<(unsigned)grid, C::THREADS, smem, stream>>>(
-        X, B, L, b0, S, s_ld, s_col0, g, g_ld, g_col0, partial);
+    kern<<<(unsigned)grid, C::THREADS, smem, stream>>>(X, B, L, b0, S, s_ld, s_col0, g, g_ld, g_col0, partial);
     timing_end(1, stream);
     SIGB_CUDA_TRY(cudaGetLastError());
     const int64_t n = Bc * L * D;

@@ -417,7 +417,7 @@ struct RedGeom {
 
 // Backward.  grid: one CTA per (CTA-part of a path) -- paths [b0, b0 + nb).
 // partial layout: [(b - b0) * CPP + cip][M][D].
-template <typename T, int D, int N, int G>
+template <typename T, int D, int N, int G, bool ASYNC = (D >= 16)>
 __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
     trunc_backward_kernel(const T* __restrict__ X, int64_t B, int64_t L, int64_t b0, const T* __restrict__ Sin,
                           int64_t s_ld, int64_t s_col0, const T* __restrict__ gup, int64_t g_ld, int64_t g_col0,
@@ -491,9 +491,7 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
     }
   }
   const int nchunks = (int)((M + kChunkT - 1) / kChunkT);
-  // asynchronous double-buffered staging measured faster at D = 16 (config 5,
-  // 406.8 vs 413.9 ms) and slower at D = 8 (config 2, 11.78 vs 11.00 ms)
-  constexpr bool ASYNC = D >= 16;
+  // ASYNC: double-buffered cp.async staging of chunk c-1 while chunk c computes
   if (ASYNC && nchunks > 0)
     issue_samples<T, D, C::PPC>(X, b_first, B, L, (nchunks - 1) * kChunkT,
                                 (int)(M - (nchunks - 1) * kChunkT), Xs);
