@@ -28,7 +28,7 @@
 namespace sigb {
 namespace trunc {
 
-constexpr int kChunkT = 16;  // steps staged per chunk
+constexpr int kChunkT = 32;  // backward steps staged per chunk (16 where the reduction buffers would not fit)
 constexpr int kThreadsT = 256;
 
 __host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
@@ -112,7 +112,7 @@ struct Frag {
 
 // Stage samples of paths of this CTA for steps [j0, j0+cs] and write the
 // increments dX[s][z] (s < cs) to shared memory: layout Dl[pc][s][D].
-template <typename T, int D, int PPC>
+template <typename T, int D, int PPC, int CH>
 __device__ __forceinline__ void stage_increments(const T* __restrict__ X, int64_t b_first, int64_t B, int64_t L,
                                                  int j0, int cs, T* __restrict__ Xs, T* __restrict__ Dl) {
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -120,13 +120,13 @@ __device__ __forceinline__ void stage_increments(const T* __restrict__ X, int64_
   for (int i = tid; i < PPC * rows * D; i += nt) {
     const int pc = i / (rows * D), r = i % (rows * D);
     const int64_t b = b_first + pc;
-    Xs[pc * (kChunkT + 1) * D + r] = b < B ? X[(b * L + j0) * D + r] : T(0);
+    Xs[pc * (CH + 1) * D + r] = b < B ? X[(b * L + j0) * D + r] : T(0);
   }
   __syncthreads();
   for (int i = tid; i < PPC * cs * D; i += nt) {
     const int pc = i / (cs * D), r = i % (cs * D);
-    const T* xs = Xs + pc * (kChunkT + 1) * D;
-    Dl[pc * kChunkT * D + r] = xs[r + D] - xs[r];
+    const T* xs = Xs + pc * (CH + 1) * D;
+    Dl[pc * CH * D + r] = xs[r + D] - xs[r];
   }
   __syncthreads();
 }
@@ -134,14 +134,14 @@ __device__ __forceinline__ void stage_increments(const T* __restrict__ X, int64_
 // Backward staging, asynchronous: element cp.async of the samples of steps
 // [j0, j0+cs] into Xb (layout of stage_increments); one commit group.  The
 // backward issues chunk c-1 while chunk c computes.
-template <typename T, int D, int PPC>
+template <typename T, int D, int PPC, int CH>
 __device__ __forceinline__ void issue_samples(const T* __restrict__ X, int64_t b_first, int64_t B, int64_t L, int j0,
                                               int cs, T* __restrict__ Xb) {
   const int rows = cs + 1;
   for (int i = threadIdx.x; i < PPC * rows * D; i += blockDim.x) {
     const int pc = i / (rows * D), r = i % (rows * D);
     const int64_t b = b_first + pc;
-    T* dst = Xb + pc * (kChunkT + 1) * D + r;
+    T* dst = Xb + pc * (CH + 1) * D + r;
     if (b < B) {
       const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
       if (sizeof(T) == 4)
@@ -406,12 +406,18 @@ struct RedGeom {
   static constexpr int RGW = 32 / C::RW;                              // reduction groups per warp
   static constexpr int NE = C::NW * RGW * GPW * (C::NC > 0 ? C::NC : 1);  // chain terms per parked step
   static constexpr int NKEY = C::PPC * D;                                 // (path slot, letter)
+  // reduction-buffer elements for a chunk of ch steps (+ staging)
+  static constexpr size_t elems(int ch) {
+    return (size_t)C::PPC * (ch + 1) * D * 2 + (size_t)C::PPC * ch * D + (size_t)C::NW * RGW * ch * D +
+           (size_t)C::NW * RGW * ch * GPW * (C::NC > 0 ? C::NC : 1);
+  }
+  static constexpr int CH = elems(kChunkT) * 8 <= 160 * 1024 ? kChunkT : 16;  // steps per chunk
   template <typename T>
   static constexpr size_t smem_bytes() {
-    return sizeof(T) * ((size_t)C::PPC * (kChunkT + 1) * D + (size_t)C::PPC * kChunkT * D +
-                        (size_t)C::NW * RGW * kChunkT * D + (size_t)C::NW * RGW * kChunkT * GPW * (C::NC > 0 ? C::NC : 1)) +
+    return sizeof(T) * ((size_t)C::PPC * (CH + 1) * D + (size_t)C::PPC * CH * D +
+                        (size_t)C::NW * RGW * CH * D + (size_t)C::NW * RGW * CH * GPW * (C::NC > 0 ? C::NC : 1)) +
            sizeof(int) * (NKEY + 1) + sizeof(unsigned short) * NE + 16 +
-           sizeof(T) * (size_t)C::PPC * (kChunkT + 1) * D;  // second sample buffer (async staging)
+           sizeof(T) * (size_t)C::PPC * (CH + 1) * D;  // second sample buffer (async staging)
   }
 };
 
@@ -428,15 +434,15 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
   constexpr int NCc = NC > 0 ? NC : 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Xs = reinterpret_cast<T*>(smem_raw);
-  T* Dl = Xs + C::PPC * (kChunkT + 1) * D;
+  T* Dl = Xs + C::PPC * (RG::CH + 1) * D;
   // per-warp per-step reduced gradients: leaf/mid letters, and chain terms per gp group
-  T(*red_leaf)[RG::RGW][kChunkT][D] = reinterpret_cast<T(*)[RG::RGW][kChunkT][D]>(Dl + C::PPC * kChunkT * D);
-  T(*red_chain)[RG::RGW][kChunkT][RG::GPW][NCc] = reinterpret_cast<T(*)[RG::RGW][kChunkT][RG::GPW][NCc]>(
-      Dl + C::PPC * kChunkT * D + C::NW * RG::RGW * kChunkT * D);
+  T(*red_leaf)[RG::RGW][RG::CH][D] = reinterpret_cast<T(*)[RG::RGW][RG::CH][D]>(Dl + C::PPC * RG::CH * D);
+  T(*red_chain)[RG::RGW][RG::CH][RG::GPW][NCc] = reinterpret_cast<T(*)[RG::RGW][RG::CH][RG::GPW][NCc]>(
+      Dl + C::PPC * RG::CH * D + C::NW * RG::RGW * RG::CH * D);
   // per-(path slot, letter) lists of this CTA's parked chain terms, built once:
   // replaces a per-element scan of every chain term in the chunk epilogue
-  int* key_off = reinterpret_cast<int*>(Dl + C::PPC * kChunkT * D + C::NW * RG::RGW * kChunkT * D +
-                                        C::NW * RG::RGW * kChunkT * RG::GPW * NCc);
+  int* key_off = reinterpret_cast<int*>(Dl + C::PPC * RG::CH * D + C::NW * RG::RGW * RG::CH * D +
+                                        C::NW * RG::RGW * RG::CH * RG::GPW * NCc);
   unsigned short* key_idx = reinterpret_cast<unsigned short*>(key_off + RG::NKEY + 1);
   T* Xs2 = reinterpret_cast<T*>(
       smem_raw + ((((size_t)(reinterpret_cast<unsigned char*>(key_idx + RG::NE) - smem_raw)) + 15) & ~size_t(15)));
@@ -487,32 +493,32 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
     for (int e = 0; e < RG::NE; ++e) {
       const int k = e % NCc, gg = (e / NCc) % RG::GPW, wr = e / (NCc * RG::GPW);
       // offset of red_chain[w][r][0][gg][k]
-      key_idx[fill[key_of(e)]++] = (unsigned short)((wr * kChunkT * RG::GPW + gg) * NCc + k);
+      key_idx[fill[key_of(e)]++] = (unsigned short)((wr * RG::CH * RG::GPW + gg) * NCc + k);
     }
   }
-  const int nchunks = (int)((M + kChunkT - 1) / kChunkT);
+  const int nchunks = (int)((M + RG::CH - 1) / RG::CH);
   // ASYNC: double-buffered cp.async staging of chunk c-1 while chunk c computes
   if (ASYNC && nchunks > 0)
-    issue_samples<T, D, C::PPC>(X, b_first, B, L, (nchunks - 1) * kChunkT,
-                                (int)(M - (nchunks - 1) * kChunkT), Xs);
+    issue_samples<T, D, C::PPC, RG::CH>(X, b_first, B, L, (nchunks - 1) * RG::CH,
+                                (int)(M - (nchunks - 1) * RG::CH), Xs);
   for (int c = nchunks - 1; c >= 0; --c) {
-    const int j0 = c * kChunkT;
-    const int cs = (int)(M - j0 < kChunkT ? M - j0 : kChunkT);
+    const int j0 = c * RG::CH;
+    const int cs = (int)(M - j0 < RG::CH ? M - j0 : RG::CH);
     if constexpr (ASYNC) {
       T* Xb = ((nchunks - 1 - c) & 1) ? Xs2 : Xs;
       asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncthreads();  // chunk c landed (every thread's copies); Dl free
       for (int i = threadIdx.x; i < C::PPC * cs * D; i += blockDim.x) {
         const int pc = i / (cs * D), r = i % (cs * D);
-        const T* xs = Xb + pc * (kChunkT + 1) * D;
-        Dl[pc * kChunkT * D + r] = xs[r + D] - xs[r];
+        const T* xs = Xb + pc * (RG::CH + 1) * D;
+        Dl[pc * RG::CH * D + r] = xs[r + D] - xs[r];
       }
       __syncthreads();
-      if (c > 0) issue_samples<T, D, C::PPC>(X, b_first, B, L, j0 - kChunkT, kChunkT, Xb == Xs ? Xs2 : Xs);
+      if (c > 0) issue_samples<T, D, C::PPC, RG::CH>(X, b_first, B, L, j0 - RG::CH, RG::CH, Xb == Xs ? Xs2 : Xs);
     } else {
-      stage_increments<T, D, C::PPC>(X, b_first, B, L, j0, cs, Xs, Dl);
+      stage_increments<T, D, C::PPC, RG::CH>(X, b_first, B, L, j0, cs, Xs, Dl);
     }
-    const T* rows = Dl + f.pc * kChunkT * D;
+    const T* rows = Dl + f.pc * RG::CH * D;
 #pragma unroll 1
     for (int s = cs - 1; s >= 0; --s) {
       StepIncr<T, D, N, G> in;
