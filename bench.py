@@ -64,6 +64,7 @@ def parse_args(argv=None):
     p.add_argument("--batch", type=int, default=0, help="override the per-rank batch (profiling only)")
     p.add_argument("--strong", action="store_true", help="shard a fixed global batch instead of per-rank batches")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--e2e-split", type=int, default=4, help="sub-batches per e2e step (copy/compute pipeline)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--gather", action="store_true", help="also time the optional NCCL all-gather of S")
     p.add_argument("--policy", type=int, default=0, help="0 auto kernels, 1 generic trie kernels only")
@@ -442,13 +443,18 @@ def run_ours(args) -> None:
         del X
         torch.cuda.empty_cache()
         readout = torch.randn((W,), generator=gen, dtype=tdt, device=dev)
-        # Two pinned result buffers and two device input buffers: step k+1's H2D (own
-        # stream) and step k's D2H (own stream) overlap step k's compute, as a training
-        # loop would pipeline them; every step still copies its inputs in and its
-        # dL/dX and loss out inside the timed region.
-        dXh = [torch.empty_like(Xh).pin_memory() for _ in range(2)]
-        lossh = torch.empty((2,), dtype=tdt).pin_memory()
-        Xbuf = [torch.empty(Xh.shape, dtype=tdt, device=dev) for _ in range(2)]
+        # A step is the whole batch as `split` sub-batches pushed through a copy /
+        # compute / copy pipeline, as a training loop would stream micro-batches:
+        # sub-batch u+1's H2D (own stream) and u-1's D2H (own stream) overlap u's
+        # compute.  Every sub-batch's inputs go in and its dL/dX and loss come out
+        # inside the timed region; only the first H2D and the last D2H of the run
+        # are exposed.
+        split = max(1, min(args.e2e_split, B))
+        bounds_u = [(B * i // split, B * (i + 1) // split) for i in range(split)]
+        ub = max(hi - lo for lo, hi in bounds_u)
+        dXh = torch.empty_like(Xh).pin_memory()
+        lossh = torch.empty((args.steps + 4, split), dtype=tdt).pin_memory()
+        Xbuf = [torch.empty((ub,) + tuple(Xh.shape[1:]), dtype=tdt, device=dev) for _ in range(2)]
         main = torch.cuda.current_stream(dev)
         h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         ready = [torch.cuda.Event() for _ in range(2)]
@@ -456,32 +462,37 @@ def run_ours(args) -> None:
         fin = torch.cuda.Event()
 
         def e2e_run(nsteps, start_ev=None):
-            def issue(k):
+            units = [(k, i) for k in range(nsteps) for i in range(split)]
+
+            def issue(u):
+                lo, hi = bounds_u[units[u][1]]
                 with torch.cuda.stream(h2d):
-                    if start_ev is not None and k == 0:
+                    if start_ev is not None and u == 0:
                         h2d.wait_event(start_ev)
-                    if k >= 2:
-                        h2d.wait_event(freed[k % 2])  # step k-2 no longer reads this buffer
-                    Xbuf[k % 2].copy_(Xh, non_blocking=True)
-                    ready[k % 2].record(h2d)
+                    if u >= 2:
+                        h2d.wait_event(freed[u % 2])  # unit u-2 no longer reads this buffer
+                    Xbuf[u % 2][: hi - lo].copy_(Xh[lo:hi], non_blocking=True)
+                    ready[u % 2].record(h2d)
 
             issue(0)
-            for k in range(nsteps):
-                if k + 1 < nsteps:
-                    issue(k + 1)
-                main.wait_event(ready[k % 2])
-                Xd = Xbuf[k % 2].detach().requires_grad_(True)
+            for u, (k, i) in enumerate(units):
+                lo, hi = bounds_u[i]
+                if u + 1 < len(units):
+                    issue(u + 1)
+                main.wait_event(ready[u % 2])
+                Xd = Xbuf[u % 2][: hi - lo].detach().requires_grad_(True)
                 Sd = sk.signature(Xd, ws)
                 loss = (Sd @ readout).sum()
                 loss.backward()
                 grad = Xd.grad
-                freed[k % 2].record(main)
+                freed[u % 2].record(main)
                 with torch.cuda.stream(d2h):
-                    d2h.wait_event(freed[k % 2])
-                    dXh[k % 2].copy_(grad, non_blocking=True)
-                    lossh[k % 2].copy_(loss.detach(), non_blocking=True)
+                    d2h.wait_event(freed[u % 2])
+                    dXh[lo:hi].copy_(grad, non_blocking=True)
+                    lossh[k, i].copy_(loss.detach(), non_blocking=True)
                 grad.record_stream(d2h)
                 loss.record_stream(d2h)
+                del Sd, loss, grad, Xd
             fin.record(d2h)
             main.wait_event(fin)
 
@@ -497,10 +508,10 @@ def run_ours(args) -> None:
         ems = max_over_ranks(a.elapsed_time(b)) / args.steps
         e2e = {"value": paths_step / (ems / 1e3), "unit": "paths/s", "ms_per_step": ems,
                "h2d_bytes_per_step": int(Xh.numel() * Xh.element_size()),
-               "d2h_bytes_per_step": int(dXh[0].numel() * dXh[0].element_size() + lossh.element_size()),
+               "d2h_bytes_per_step": int(dXh.numel() * dXh.element_size() + split * lossh.element_size()),
                "api": "paper_2602_24066_b200.signature (autograd) on pinned host paths; loss = (S @ r).sum(); "
-                      "dL/dX and loss copied back; H2D / D2H on their own streams, overlapping the "
-                      "neighbouring steps' compute"}
+                      "dL/dX and loss copied back; the batch streams as %d sub-batches with H2D / D2H on their "
+                      "own streams overlapping the neighbouring sub-batches' compute" % split}
         # forward through the numpy drop-in (signature_forward: host array in, host array out)
         Bn = min(B, max(1, (8 << 30) // (W * s_el)))
         Xn = Xh[:Bn].numpy()
