@@ -67,6 +67,11 @@ def precompile_shipped() -> None:
     words = os.path.join(os.path.dirname(HERE), "tests", "golden", "c3_words.json")
     if not os.path.exists(words):
         return
+    cache = os.path.join(HERE, "jit_cache")
+    if os.path.isdir(cache):  # drop cubins of earlier generator versions
+        for name in os.listdir(cache):
+            if name.endswith(".cubin"):
+                os.remove(os.path.join(cache, name))
     with open(words) as f:
         ws = build_custom([tuple(w) for w in json.load(f)["words"]], 16)
     for backward in (False, True):

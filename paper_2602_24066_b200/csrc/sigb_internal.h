@@ -119,6 +119,7 @@ struct Task {
 struct Cfg {
   int warps = 4, ch = 8, minb = 4, pb = 1;
   int lock = 0;  // slots claim together and share the CTA barrier (lockstep)
+  int maxreg = 0;  // NVRTC --maxrregcount (0: launch bounds only)
   int64_t cap = 96;
 };
 }  // namespace jit

@@ -75,6 +75,7 @@ Cfg default_cfg(int dtype, int d, bool backward) {
     c.cap = env_int("SIGB_JIT_BCAP", 96);
     c.pb = env_int("SIGB_JIT_BPB", 2);
     c.lock = env_int("SIGB_JIT_BLOCK", 1);
+    c.maxreg = env_int("SIGB_JIT_BMAXREG", 184);  // measured best on config 3 (2.98 vs 3.12 ms uncapped)
   }
   c.warps = std::min(std::max(c.warps, 1), 16);
   c.ch = std::min(std::max(c.ch, 1), 64);
@@ -287,6 +288,7 @@ std::string common_head(int dtype, int d, const Cfg& c) {
   o << "typedef " << tname(dtype) << " R;\n";
   o << "#define D " << d << "\n#define CH " << c.ch << "\n#define WARPS " << c.warps << "\n#define NT (32 * WARPS)\n";
   o << "#define PB " << c.pb << "\n#define LOCK " << c.lock << "\n";
+  if (c.maxreg > 0) o << "// maxrregcount " << c.maxreg << "\n";
   o << "#define MINB " << c.minb << "\n#define VW " << vw << "\n#define PITCH " << pitch(dtype, d, c.ch) << "\n";
   o << R"(
 struct __align__(VW * sizeof(R)) RV { R v[VW]; };
@@ -708,7 +710,9 @@ void mkdirs(const std::string& path) {
 
 // NVRTC -> cubin for sm_100a (cached on disk by a hash of the source).
 int compile(const std::string& src, std::string& cubin) {
-  const std::string key = std::to_string(std::hash<std::string>{}(src)) + "_" + std::to_string(src.size());
+  const char* xo = getenv("SIGB_JIT_NVRTC_OPTS");
+  const std::string keysrc = xo ? src + "\n// opts: " + xo : src;
+  const std::string key = std::to_string(std::hash<std::string>{}(keysrc)) + "_" + std::to_string(src.size());
   const std::vector<std::string> dirs = cache_dirs();
   for (const std::string& dir : dirs) {
     std::ifstream in(dir + "/" + key + ".cubin", std::ios::binary);
@@ -720,8 +724,18 @@ int compile(const std::string& src, std::string& cubin) {
   nvrtcProgram prog;
   if (nvrtcCreateProgram(&prog, src.c_str(), "sigb_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
     return fail(SIGB_ERR_CUDA, "nvrtcCreateProgram failed");
-  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-default-device", "-lineinfo"};
-  nvrtcResult rc = nvrtcCompileProgram(prog, 4, opts);
+  // SIGB_JIT_NVRTC_OPTS: extra space-separated NVRTC options (sweeps only; part of the cache key)
+  std::vector<std::string> extra;
+  if (const char* e = getenv("SIGB_JIT_NVRTC_OPTS")) {
+    std::istringstream is(e);
+    for (std::string w; is >> w;) extra.push_back(w);
+  }
+  // a register cap chosen by the generator travels in the source ("// maxrregcount N")
+  const size_t mr = src.find("// maxrregcount ");
+  if (mr != std::string::npos) extra.push_back("--maxrregcount=" + std::to_string(atoi(src.c_str() + mr + 16)));
+  std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "--std=c++17", "-default-device", "-lineinfo"};
+  for (const std::string& w : extra) opts.push_back(w.c_str());
+  nvrtcResult rc = nvrtcCompileProgram(prog, (int)opts.size(), opts.data());
   if (rc != NVRTC_SUCCESS) {
     size_t n = 0;
     nvrtcGetProgramLogSize(prog, &n);

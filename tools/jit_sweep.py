@@ -19,15 +19,16 @@ import paper_2602_24066_b200 as sk  # noqa: E402
 from oracle import oracle as ora  # noqa: E402  (checker only)
 from tests.configs import brownian, c3_words  # noqa: E402
 
-KEYS = ("FWARPS", "FCH", "FMINB", "FCAP", "FPB", "BWARPS", "BCH", "BMINB", "BCAP", "BPB", "FLOCK", "BLOCK")
+KEYS = ("FWARPS", "FCH", "FMINB", "FCAP", "FPB", "BWARPS", "BCH", "BMINB", "BCAP", "BPB", "FLOCK", "BLOCK", "BMAXREG")
 
 
 def run(B, setting, reps=5):
     for k in KEYS:
         os.environ.pop("SIGB_JIT_" + k, None)
+    os.environ.pop("SIGB_JIT_NVRTC_OPTS", None)
     for kv in filter(None, setting.split(",")):
-        k, v = kv.split("=")
-        os.environ["SIGB_JIT_" + k] = v
+        k, v = kv.split("=", 1)
+        os.environ["SIGB_JIT_" + k] = v.replace("+", " ")
     ws = sk.build_custom(c3_words(), 16)
     plan = ws.plan()
     assert plan.kernel_kind == 4, plan.kernel_kind
