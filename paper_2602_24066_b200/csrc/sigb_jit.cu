@@ -68,6 +68,7 @@ Cfg default_cfg(int dtype, int d, bool backward) {
     c.cap = env_int("SIGB_JIT_FCAP", 96);
     c.pb = env_int("SIGB_JIT_FPB", 3);
     c.lock = env_int("SIGB_JIT_FLOCK", 0);
+    c.maxreg = env_int("SIGB_JIT_FMAXREG", 0);
   } else {
     c.warps = env_int("SIGB_JIT_BWARPS", 4);
     c.ch = env_int("SIGB_JIT_BCH", 8);

@@ -19,7 +19,7 @@ import paper_2602_24066_b200 as sk  # noqa: E402
 from oracle import oracle as ora  # noqa: E402  (checker only)
 from tests.configs import brownian, c3_words  # noqa: E402
 
-KEYS = ("FWARPS", "FCH", "FMINB", "FCAP", "FPB", "BWARPS", "BCH", "BMINB", "BCAP", "BPB", "FLOCK", "BLOCK", "BMAXREG")
+KEYS = ("FWARPS", "FCH", "FMINB", "FCAP", "FPB", "BWARPS", "BCH", "BMINB", "BCAP", "BPB", "FLOCK", "BLOCK", "BMAXREG", "FMAXREG")
 
 
 def run(B, setting, reps=5):
