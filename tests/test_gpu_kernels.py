@@ -252,3 +252,33 @@ def test_backward_memory_contract(name):
         assert work <= 64 * 4 * (L - 1) * d * 4  # partials: at most 64 parts x dX
         extra.append(peak - work)
     assert extra[1] <= extra[0] + (1 << 20), extra  # independent of M (1 MiB slack for the allocator)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,misaligned", [(16, False), (16, True), (10, False)])
+def test_generated_kernels_many_path_blocks(d, misaligned):
+    """Several 32-path blocks per task group (persistent claiming, lockstep slots
+    with an idle slot at the tail), partial chunks, bulk-copy staging (d*4 % 16 == 0)
+    and its element-copy fallback (d = 10, or a sample pointer off 16-byte alignment)."""
+    _lib.set_kernel_policy(4)
+    try:
+        rng = np.random.default_rng(300 + d)
+        ws = random_trie(rng, d, 4, 220)
+        assert ws.plan().kernel_kind == 4
+        B, L = 101, 45
+        X = brownian(7, B, L, d)
+        g = np.random.default_rng(8).standard_normal((B, len(ws)))
+        ref = ora.forward(X, ws.codes, ws.lengths, d)
+        _, dref = ora.backward(X, ws.codes, ws.lengths, d, g)
+        flat = torch.empty(B * L * d + 1, dtype=torch.float32, device="cuda")
+        X32 = (flat[1:] if misaligned else flat[:-1]).view(B, L, d)
+        X32.copy_(torch.from_numpy(X.astype(np.float32)))
+        X32.requires_grad_(True)
+        S32 = sk.signature(X32, ws)
+        S32.backward(torch.from_numpy(g).float().cuda())
+        assert ora.rel_err(S32.detach().cpu().numpy(), ref) <= TOL32
+        assert ora.rel_err(X32.grad.cpu().numpy(), dref) <= TOL32
+        assert ora.rel_err(sk.signature_forward(X, ws).values, ref) <= TOL64
+        assert ora.rel_err(sk.signature_backward(X, ws, g).path_grads, dref) <= TOL64
+    finally:
+        _lib.set_kernel_policy(0)
