@@ -513,7 +513,8 @@ def run_ours(args) -> None:
                       "dL/dX and loss copied back; the batch streams as %d sub-batches with H2D / D2H on their "
                       "own streams overlapping the neighbouring sub-batches' compute" % split}
         # forward through the numpy drop-in (signature_forward: host array in, host array out)
-        Bn = min(B, max(1, (8 << 30) // (W * s_el)))
+        # host result buffers are pinned: keep them to ~2 GB per rank (8 ranks share one host)
+        Bn = min(B, max(1, (2 << 30) // (W * s_el)))
         Xn = Xh[:Bn].numpy()
         del Xh, dXh, Xbuf
         torch.cuda.empty_cache()
