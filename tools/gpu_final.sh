@@ -27,6 +27,10 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:trun
   -o $O/prof_c2_bwd python bench.py --config c2 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --batch 512 > $O/ncu_c2b.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:trunc_forward -c 1 \
   -o $O/prof_c2_fwd python bench.py --config c2 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --batch 1024 > $O/ncu_c2f.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:trunc_backward -c 1 \
+  -o $O/prof_c5_bwd python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --batch 1024 > $O/ncu_c5b.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:trunc_forward -c 1 \
+  -o $O/prof_c5_fwd python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --batch 2048 > $O/ncu_c5f.log 2>&1
 for r in $O/prof_*.ncu-rep; do
   ncu -i $r --page raw --csv > ${r%.ncu-rep}.csv 2>/dev/null
   ncu -i $r --page source --csv --print-source sass > ${r%.ncu-rep}_sass.csv 2>/dev/null
