@@ -308,6 +308,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned phase)
     asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
                  : "=r"(done) : "r"(su32(m)), "r"(phase) : "memory");
   } while (!done);
+  __syncwarp();  // lanes may leave the spin at different polls: reconverge before the (aligned) barriers
 }
 __device__ __forceinline__ int stid() { return (int)threadIdx.x % (32 * WARPS); }  // thread index in the slot
 __device__ __forceinline__ int slot_id() { return (int)(threadIdx.x >> 5) / WARPS; }
@@ -315,11 +316,13 @@ __device__ __forceinline__ int slot_id() { return (int)(threadIdx.x >> 5) / WARP
 // CTA barrier, so the warps of one task on an SM scheduler stay in lockstep
 // (one instruction fetch serves both); otherwise each slot has its own
 // named barrier and runs free.
+// Non-.aligned barriers: the warps of a slot reach them from different task
+// functions (different PCs), which bar.sync / __syncthreads (.aligned) forbid.
 __device__ __forceinline__ void slot_sync() {
 #if LOCK
-  __syncthreads();
+  asm volatile("barrier.sync 0;" ::: "memory");
 #else
-  asm volatile("bar.sync %0, %1;" ::"r"(1 + slot_id()), "r"(32 * WARPS) : "memory");
+  asm volatile("barrier.sync %0, %1;" ::"r"(1 + slot_id()), "r"(32 * WARPS) : "memory");
 #endif
 }
 __device__ __forceinline__ void cp_async(R* dst, const R* src) {

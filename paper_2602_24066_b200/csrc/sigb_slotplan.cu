@@ -45,9 +45,12 @@ bool plan_slots(const Trie& t, SlotHost& out, std::string& why) {
   o += kChunkS * d * AW;
   out.t_off = o = al4(o);
   out.lvl.assign(2 * N + 4, 0);
+  // each level's T-vectors are followed by 8 pad elements: the kernels read a
+  // parent's T-vector as 8 values (ld8) and use only the first nT, so the
+  // over-read must not touch the next level while it is being written
   for (int l = 1; l <= N; ++l) {
     out.lvl[l] = o;
-    o += n[l] * t_stride(N, l);
+    o += n[l] * t_stride(N, l) + 8;
   }
   out.t_size = o - out.t_off;
   // parking: letter-major blocks padded to float4
@@ -66,7 +69,7 @@ bool plan_slots(const Trie& t, SlotHost& out, std::string& why) {
   o = al4(o);
   for (int l = 1; l <= N; ++l) {
     out.lvl[N + 2 + l] = o;
-    o += n[l] * p_stride(N, l);
+    o += n[l] * p_stride(N, l) + 8;
   }
   out.p_off = out.lvl[N + 3];
   out.p_size = o - out.p_off;

@@ -43,11 +43,14 @@ def main():
         "trunc d=8 N=5": sk.build_truncated(8, 5),
         "aniso": sk.build_anisotropic(sk.AnisotropyWeights((1.0,) * 3 + (2.0,) * 3, 5.0)),
         "custom non-closed": sk.build_custom([(0, 1, 1), (1,), (2, 2, 2, 2), (3, 0)], 4),
+        "sparse d=16 trie": sk.build_custom([(i,) for i in range(16)] + [(i, (3 * i) % 16) for i in range(16)]
+                                            + [(i, (3 * i) % 16, (5 * i + 1) % 16) for i in range(0, 16, 2)], 16),
     }
     for policy in (0, 1, 2, 3, 4):
         _lib.set_kernel_policy(policy)
         for name, ws in sets.items():
-            run(ws, B=2 if "16" in name else 3, L=24 if "16" in name else 40)
+            B = 70 if "sparse" in name else (2 if "16" in name else 3)  # sparse: several 32-path blocks
+            run(ws, B=B, L=24 if "16" in name else 40)
             print(f"policy {policy} {name}: kernel kind {ws.plan().kernel_kind}", flush=True)
     _lib.set_kernel_policy(0)
     print("sanitize workload done")
