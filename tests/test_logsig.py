@@ -189,3 +189,23 @@ def test_errors_and_torch_inputs():
     assert t.is_cuda
     np.testing.assert_allclose(t.cpu().numpy(), sk.logsignature_forward(X.cpu().numpy(), 3, 4).values, rtol=0,
                                atol=0)
+
+
+@pytest.mark.gpu
+def test_batches_beyond_one_grid_row():
+    """More than 65,535 paths: the polynomial and tensor-product launches split the batch."""
+    rng = np.random.default_rng(67)
+    B = 70_001
+    X = rng.random((B, 3, 2)) * 2 - 1
+    out = sk.logsignature_forward(X, 2, 2).values
+    ly = sk.build_lyndon(2, 2)
+    rows = [0, 1, 65_534, 65_535, 65_536, B - 1]
+    ref = ora.lyndon_logsig(X[rows], 2, 2, ly.codes, ly.lengths)
+    assert ora.rel_err(out[rows], ref) <= 1e-12
+    ws = sk.build_truncated(2, 2)
+    S = sk.signature_forward(X, ws)
+    assert ora.rel_err(sk.tensor_log(S).values[rows], ora.dense_log(S.values[rows], 2, 2)) <= 1e-12
+    g = rng.standard_normal((B, len(ly)))
+    dX = sk.logsignature_backward(X, 2, 2, g).path_grads
+    # level-one letters: dL/dX_0 = -g, dL/dX_M = +g for the displacement part; check finite and shaped
+    assert dX.shape == X.shape and np.isfinite(dX).all()
