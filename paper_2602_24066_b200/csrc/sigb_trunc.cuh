@@ -399,6 +399,40 @@ __device__ __forceinline__ int transpose_reduce(T (&v)[V], int lane) {
   return idx;
 }
 
+// The same reduction for 16 values over 32 lanes whose registers are
+// XOR-permuted by f = 8*bit4(lane) + 4*bit3(lane) (register p holds letter
+// p ^ f): the first two stages then keep the low half and send the high half
+// in every lane -- no select pairs -- and leave letters f..f+3 in v[0..3].
+template <typename T>
+__device__ __forceinline__ int transpose_reduce_perm16(T (&v)[16], int lane) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] += shfl_xor(v[i + 8], 16);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] += shfl_xor(v[i + 4], 8);
+  int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4;
+  int cnt = 4;
+#pragma unroll
+  for (int mask = 4; mask >= 1; mask /= 2) {
+    if (cnt > 1) {
+      const int half = cnt / 2;
+      const bool upper = (lane & mask) != 0;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        if (i < half) {
+          const T send = upper ? v[i] : v[i + half];
+          const T keep = upper ? v[i + half] : v[i];
+          v[i] = keep + shfl_xor(send, mask);
+        }
+      }
+      if (upper) idx += half;
+      cnt = half;
+    } else {
+      v[0] += shfl_xor(v[0], mask);
+    }
+  }
+  return idx;
+}
+
 template <int D, int N, int G>
 struct RedGeom {
   using C = Cfg<D, N, G>;
@@ -454,6 +488,10 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rg = lane / C::RW;  // reduction group inside the warp
   State<T, D, N, G> st, lam;
+  // PERM (D = 16 over full warps): leaf-letter registers XOR-permuted per lane so
+  // the gradient butterfly's first two stages need no selects (transpose_reduce_perm16)
+  constexpr bool PERM = D == 16 && C::RW == 32 && G == 4 && sizeof(T) == 4;
+  const int pperm = PERM ? ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 : 0;
   // terminal state and adjoint seeds
   {
     const T* srow = Sin + (live ? f.b : 0) * s_ld + s_col0;
@@ -470,7 +508,7 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
 #pragma unroll
       for (int z = 0; z < D; ++z) {
         st.leaf[g][z] = T(0);  // never read by the backward
-        lam.leaf[g][z] = live ? grow[f.leaf_index(g, z)] : T(0);
+        lam.leaf[g][z] = live ? grow[f.leaf_index(g, PERM ? (z ^ pperm) : z)] : T(0);
       }
     }
   }
@@ -524,6 +562,14 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
       StepIncr<T, D, N, G> in;
       // (a) rebuild S_{0,t_j} = S_{0,t_{j+1}} ⊗ exp(-dX_j) (chain and mids only)
       in.load(rows + s * D, f, T(-1));
+      if constexpr (PERM) {  // leaf increments in the lane's permuted letter order (quad-level XOR)
+        const T* row = rows + s * D;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float4 q4 = *reinterpret_cast<const float4*>(row + 4 * (k ^ (pperm >> 2)));
+          in.dz[4 * k] = -q4.x; in.dz[4 * k + 1] = -q4.y; in.dz[4 * k + 2] = -q4.z; in.dz[4 * k + 3] = -q4.w;
+        }
+      }
       chen_step<T, D, N, G, false>(st, in);
       // (b) forward partials from S_{0,t_j}
 #pragma unroll
@@ -587,7 +633,7 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
 #pragma unroll
         for (int qq = 0; qq < C::Q; ++qq)
 #pragma unroll
-          for (int g = 0; g < G; ++g) gl[qq * G + g] += (f.q == qq) ? gm[g] : T(0);
+          for (int g = 0; g < G; ++g) gl[qq * G + g] += ((f.q ^ (PERM ? (pperm >> 2) : 0)) == qq) ? gm[g] : T(0);
       }
       // chain, deepest first: tbc[m] = Tbar(node, m) contributed by its child
       T gch[NCc];
@@ -619,7 +665,9 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
         }
       }
       // (d) reduce within the path's lanes; park per-warp results in shared memory
-      const int idx = transpose_reduce<T, D, C::RW>(gl, lane);
+      int idx;
+      if constexpr (PERM) idx = transpose_reduce_perm16<T>(reinterpret_cast<T(&)[16]>(gl), lane);
+      else idx = transpose_reduce<T, D, C::RW>(gl, lane);
       constexpr int plain_bits = C::RW / (D < C::RW ? D : C::RW);  // lanes sharing one letter
       if ((lane % C::RW) % plain_bits == 0 && D <= C::RW) red_leaf[warp][rg][s][idx] = gl[0];
 #pragma unroll
