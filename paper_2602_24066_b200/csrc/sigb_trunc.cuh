@@ -400,36 +400,36 @@ __device__ __forceinline__ int transpose_reduce(T (&v)[V], int lane) {
 }
 
 // The same reduction for 16 values over 32 lanes whose registers are
-// XOR-permuted by f = 8*bit4(lane) + 4*bit3(lane) (register p holds letter
-// p ^ f): the first two stages then keep the low half and send the high half
-// in every lane -- no select pairs -- and leave letters f..f+3 in v[0..3].
+// XOR-permuted by f = 4 * (lane & 3) (register p holds letter p ^ f): the
+// stages over lane bits 1 and 0 then keep the low half and send the high half
+// in every lane -- no select pairs -- and leave letters f..f+3 in v[0..3];
+// bits 4, 3 and 2 finish as in transpose_reduce.  With G = 4 a thread's mid
+// letters (quad lane & 3) sit in registers 0..3 of that order.
 template <typename T>
 __device__ __forceinline__ int transpose_reduce_perm16(T (&v)[16], int lane) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] += shfl_xor(v[i + 8], 16);
+  for (int i = 0; i < 8; ++i) v[i] += shfl_xor(v[i + 8], 2);
 #pragma unroll
-  for (int i = 0; i < 4; ++i) v[i] += shfl_xor(v[i + 4], 8);
-  int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4;
-  int cnt = 4;
+  for (int i = 0; i < 4; ++i) v[i] += shfl_xor(v[i + 4], 1);
+  int idx = 4 * (lane & 3);
+  {
+    const bool upper = (lane & 16) != 0;
 #pragma unroll
-  for (int mask = 4; mask >= 1; mask /= 2) {
-    if (cnt > 1) {
-      const int half = cnt / 2;
-      const bool upper = (lane & mask) != 0;
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        if (i < half) {
-          const T send = upper ? v[i] : v[i + half];
-          const T keep = upper ? v[i + half] : v[i];
-          v[i] = keep + shfl_xor(send, mask);
-        }
-      }
-      if (upper) idx += half;
-      cnt = half;
-    } else {
-      v[0] += shfl_xor(v[0], mask);
+    for (int i = 0; i < 2; ++i) {
+      const T send = upper ? v[i] : v[i + 2];
+      const T keep = upper ? v[i + 2] : v[i];
+      v[i] = keep + shfl_xor(send, 16);
     }
+    if (upper) idx += 2;
   }
+  {
+    const bool upper = (lane & 8) != 0;
+    const T send = upper ? v[0] : v[1];
+    const T keep = upper ? v[1] : v[0];
+    v[0] = keep + shfl_xor(send, 8);
+    if (upper) idx += 1;
+  }
+  v[0] += shfl_xor(v[0], 4);
   return idx;
 }
 
@@ -488,10 +488,11 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rg = lane / C::RW;  // reduction group inside the warp
   State<T, D, N, G> st, lam;
-  // PERM (D = 16 over full warps): leaf-letter registers XOR-permuted per lane so
-  // the gradient butterfly's first two stages need no selects (transpose_reduce_perm16)
-  constexpr bool PERM = D == 16 && C::RW == 32 && G == 4 && sizeof(T) == 4;
-  const int pperm = PERM ? ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 : 0;
+  // PERM (D = 16, G = 4, full warps of one path): leaf-letter registers XOR-permuted
+  // per lane so the gradient butterfly's first two stages need no selects and the
+  // thread's mid letters land in registers 0..3 (transpose_reduce_perm16)
+  constexpr bool PERM = D == 16 && C::RW == 32 && G == 4 && C::Q == 4 && sizeof(T) == 4;
+  const int pperm = PERM ? 4 * (lane & 3) : 0;
   // terminal state and adjoint seeds
   {
     const T* srow = Sin + (live ? f.b : 0) * s_ld + s_col0;
@@ -629,11 +630,14 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
       if constexpr (G == D) {
 #pragma unroll
         for (int g = 0; g < G; ++g) gl[g] += gm[g];
+      } else if constexpr (PERM) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) gl[g] += gm[g];  // letter quad f.q = lane & 3 sits at registers 0..3
       } else {
 #pragma unroll
         for (int qq = 0; qq < C::Q; ++qq)
 #pragma unroll
-          for (int g = 0; g < G; ++g) gl[qq * G + g] += ((f.q ^ (PERM ? (pperm >> 2) : 0)) == qq) ? gm[g] : T(0);
+          for (int g = 0; g < G; ++g) gl[qq * G + g] += (f.q == qq) ? gm[g] : T(0);
       }
       // chain, deepest first: tbc[m] = Tbar(node, m) contributed by its child
       T gch[NCc];
@@ -669,7 +673,9 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
       if constexpr (PERM) idx = transpose_reduce_perm16<T>(reinterpret_cast<T(&)[16]>(gl), lane);
       else idx = transpose_reduce<T, D, C::RW>(gl, lane);
       constexpr int plain_bits = C::RW / (D < C::RW ? D : C::RW);  // lanes sharing one letter
-      if ((lane % C::RW) % plain_bits == 0 && D <= C::RW) red_leaf[warp][rg][s][idx] = gl[0];
+      // one writer per letter: the plain (duplicating) stage is lane bit 2 for PERM, bit 0 otherwise
+      const bool writer = PERM ? (lane & 4) == 0 : (lane % C::RW) % plain_bits == 0;
+      if (writer && D <= C::RW) red_leaf[warp][rg][s][idx] = gl[0];
 #pragma unroll
       for (int k = 0; k < NC; ++k) {
         T v = gch[k];
