@@ -399,19 +399,24 @@ __device__ __forceinline__ int transpose_reduce(T (&v)[V], int lane) {
   return idx;
 }
 
-// The same reduction for 16 values over 32 lanes whose registers are
-// XOR-permuted by f = 4 * (lane & 3) (register p holds letter p ^ f): the
-// stages over lane bits 1 and 0 then keep the low half and send the high half
-// in every lane -- no select pairs -- and leave letters f..f+3 in v[0..3];
-// bits 4, 3 and 2 finish as in transpose_reduce.  With G = 4 a thread's mid
-// letters (quad lane & 3) sit in registers 0..3 of that order.
-template <typename T>
-__device__ __forceinline__ int transpose_reduce_perm16(T (&v)[16], int lane) {
+// The same reduction for V = 16 or 8 values over 32 lanes whose registers
+// are XOR-permuted by f = 4 * (lane & (V/4 - 1)) (register p holds letter
+// p ^ f): the stages over the low lane bits then keep the low half and send
+// the high half in every lane -- no select pairs -- and leave letters
+// f..f+3 in v[0..3]; lane bits 4 and 3 finish with selects, the remaining
+// bits are plain sums (lanes differing only there hold the same letter).
+// With G = 4 a thread's mid letters (quad lane & (V/4 - 1)) sit in
+// registers 0..3 of that order.
+template <typename T, int V>
+__device__ __forceinline__ int transpose_reduce_perm(T (&v)[V], int lane) {
+  static_assert(V == 16 || V == 8, "quad-permuted butterfly for 8 or 16 letters");
+  if constexpr (V == 16) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] += shfl_xor(v[i + 8], 2);
+    for (int i = 0; i < 8; ++i) v[i] += shfl_xor(v[i + 8], 2);
+  }
 #pragma unroll
   for (int i = 0; i < 4; ++i) v[i] += shfl_xor(v[i + 4], 1);
-  int idx = 4 * (lane & 3);
+  int idx = 4 * (lane & (V / 4 - 1));
   {
     const bool upper = (lane & 16) != 0;
 #pragma unroll
@@ -430,6 +435,7 @@ __device__ __forceinline__ int transpose_reduce_perm16(T (&v)[16], int lane) {
     if (upper) idx += 1;
   }
   v[0] += shfl_xor(v[0], 4);
+  if constexpr (V == 8) v[0] += shfl_xor(v[0], 2);
   return idx;
 }
 
@@ -491,8 +497,8 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
   // PERM (D = 16, G = 4, full warps of one path): leaf-letter registers XOR-permuted
   // per lane so the gradient butterfly's first two stages need no selects and the
   // thread's mid letters land in registers 0..3 (transpose_reduce_perm16)
-  constexpr bool PERM = D == 16 && C::RW == 32 && G == 4 && C::Q == 4 && sizeof(T) == 4;
-  const int pperm = PERM ? 4 * (lane & 3) : 0;
+  constexpr bool PERM = (D == 16 || D == 8) && C::RW == 32 && G == 4 && C::Q == D / 4 && sizeof(T) == 4;
+  const int pperm = PERM ? 4 * (lane & (D / 4 - 1)) : 0;
   // terminal state and adjoint seeds
   {
     const T* srow = Sin + (live ? f.b : 0) * s_ld + s_col0;
@@ -566,7 +572,7 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
       if constexpr (PERM) {  // leaf increments in the lane's permuted letter order (quad-level XOR)
         const T* row = rows + s * D;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < D / 4; ++k) {
           const float4 q4 = *reinterpret_cast<const float4*>(row + 4 * (k ^ (pperm >> 2)));
           in.dz[4 * k] = -q4.x; in.dz[4 * k + 1] = -q4.y; in.dz[4 * k + 2] = -q4.z; in.dz[4 * k + 3] = -q4.w;
         }
@@ -670,11 +676,12 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
       }
       // (d) reduce within the path's lanes; park per-warp results in shared memory
       int idx;
-      if constexpr (PERM) idx = transpose_reduce_perm16<T>(reinterpret_cast<T(&)[16]>(gl), lane);
+      if constexpr (PERM) idx = transpose_reduce_perm<T, D>(gl, lane);
       else idx = transpose_reduce<T, D, C::RW>(gl, lane);
       constexpr int plain_bits = C::RW / (D < C::RW ? D : C::RW);  // lanes sharing one letter
-      // one writer per letter: the plain (duplicating) stage is lane bit 2 for PERM, bit 0 otherwise
-      const bool writer = PERM ? (lane & 4) == 0 : (lane % C::RW) % plain_bits == 0;
+      // one writer per letter: the plain (duplicating) stages are lane bits 2 (and 1 for
+      // D = 8) for PERM, the low bits otherwise
+      const bool writer = PERM ? (lane & (D == 16 ? 4 : 6)) == 0 : (lane % C::RW) % plain_bits == 0;
       if (writer && D <= C::RW) red_leaf[warp][rg][s][idx] = gl[0];
 #pragma unroll
       for (int k = 0; k < NC; ++k) {
