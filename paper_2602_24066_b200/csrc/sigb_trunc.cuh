@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
     const int64_t j1 = j0 + CH;
     if (j1 < M) pf.load(X, b_first, B, L, bounds, K, j1, (int)(M - j1 < CH ? M - j1 : CH));  // in flight during steps
     const T* rows = Dl + f.pc * CH * D;
-#pragma unroll 1
+#pragma unroll 2
     for (int s = 0; s < cs; ++s) {
       StepIncr<T, D, N, G> in;
       in.load(rows + s * D, f, T(1));
