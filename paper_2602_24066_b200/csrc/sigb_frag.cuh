@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kTPB) frag_forward_kernel(FragDev fd, const T*
     diff_rows<T>(Xc, fd.d, cs, Dl);
     const int64_t j1 = j0 + kChunkF;
     if (j1 < M) issue_rows<T>(Xb, fd.d, (int)j1, (int)(M - j1 < kChunkF ? M - j1 : kChunkF), (c & 1) ? Xs : Xs2);
-#pragma unroll 1
+#pragma unroll 2
     for (int s = 0; s < cs; ++s) {
       FIncr<T, NC, G, K> in;
       gather<T, NC, G, K>(Dl + s * (fd.d + 1), lt, T(1), in);
