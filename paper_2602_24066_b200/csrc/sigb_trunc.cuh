@@ -348,7 +348,10 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
     const int64_t j1 = j0 + CH;
     if (j1 < M) pf.load(X, b_first, B, L, bounds, K, j1, (int)(M - j1 < CH ? M - j1 : CH));  // in flight during steps
     const T* rows = Dl + f.pc * CH * D;
-#pragma unroll 2
+    // next steps' increment loads overlap this step's FMAs: by 4 at D = 16 (c5 fwd
+    // 134.0 -> 129.4 -> 127.7 ms for 1 / 2 / 4), by 2 below (c2: 4 measured slower)
+    constexpr int kUnrollF = D >= 16 ? 4 : 2;
+#pragma unroll kUnrollF
     for (int s = 0; s < cs; ++s) {
       StepIncr<T, D, N, G> in;
       in.load(rows + s * D, f, T(1));
