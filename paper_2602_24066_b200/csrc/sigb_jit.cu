@@ -53,7 +53,8 @@ int env_int(const char* name, int dflt) {
 }
 
 // Defaults measured on B200 for config 3 (r01 sweeps, tools/jit_sweep.py):
-// the forward runs 3 slots x 4 tasks per SM (12 warps, 168 registers), the
+// the forward runs 3 slots x 4 tasks per SM (12 warps, 168 registers, 16-step
+// chunks, 112-T-node tasks: 0.85 -> 0.75 ms against 12 / 96), the
 // backward 2 slots x 4 tasks (8 warps, up to 255 registers for 96-T-node
 // tasks).  Two slots of the same task on one SM scheduler share its
 // instruction cache; separate CTAs of different groups thrash it.
@@ -63,9 +64,9 @@ Cfg default_cfg(int dtype, int d, bool backward) {
   Cfg c;
   if (!backward) {
     c.warps = env_int("SIGB_JIT_FWARPS", 4);
-    c.ch = env_int("SIGB_JIT_FCH", 12);
+    c.ch = env_int("SIGB_JIT_FCH", 16);
     c.minb = env_int("SIGB_JIT_FMINB", 1);
-    c.cap = env_int("SIGB_JIT_FCAP", 96);
+    c.cap = env_int("SIGB_JIT_FCAP", 112);
     c.pb = env_int("SIGB_JIT_FPB", 3);
     c.lock = env_int("SIGB_JIT_FLOCK", 0);
     c.maxreg = env_int("SIGB_JIT_FMAXREG", 0);
