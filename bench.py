@@ -408,6 +408,9 @@ def run_ours(args) -> None:
     kb_name, kf_name = prefix + "backward_kernel", prefix + "forward_kernel"
     if plan.kernel_kind == 4:
         kb_name, kf_name = "sigjit_bwd", "sigjit_fwd"
+    if (plan.kernel_kind == 1 and cfg.get("kind") == "truncated" and d == 16 and cfg.get("depth") == 4
+            and tdt == torch.float32 and os.environ.get("SIGB_TRUNC_TC", "1") != "0"):
+        kf_name = "trunc_tc_forward_kernel"  # leaf level on the tensor cores (csrc/sigb_trunc_tc.cuh)
     roof_b = roof(kb_name, f_bwd_path, kb_ms, kb_n, bytes_bwd)
     roof_f = roof(kf_name, f_fwd_path, kf_ms, kf_n, bytes_fwd)
     dominant = roof_b if (roof_b and kb_ms >= kf_ms) else roof_f

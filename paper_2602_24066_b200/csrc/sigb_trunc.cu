@@ -4,7 +4,10 @@
 // runs the generic trie kernels of sigb_level.cu.
 #include <cstdlib>
 
+#include <type_traits>
+
 #include "sigb_trunc.cuh"
+#include "sigb_trunc_tc.cuh"
 
 namespace sigb {
 namespace trunc {
@@ -18,6 +21,20 @@ int fwd(const T* X, int64_t B, int64_t L, const int64_t* bounds, int64_t K, T* o
   using C = Cfg<D, N, G>;
   const int64_t grid = C::CPP > 1 ? B * C::CPP : (B + C::PPC - 1) / C::PPC;
   if (grid == 0) return SIGB_OK;
+  if constexpr (std::is_same<T, float>::value && D == 16 && N == 4) {
+    // leaf level on the tensor cores (sigb_trunc_tc.cuh): c5 fwd 127.4 -> 92.5 ms.
+    // SIGB_TRUNC_TC=0 selects the register kernel (A/B experiments, parity tests).
+    const char* e = getenv("SIGB_TRUNC_TC");
+    if (!(e && atoi(e) == 0) && !bounds) {
+      count_launch();
+      timing_begin(0, stream);
+      tc::trunc_tc_forward_kernel<D, N><<<(unsigned)grid, tc::kThreadsTc, 0, stream>>>(X, B, L, out, out_ld, out_col0,
+                                                                                       include_empty);
+      timing_end(0, stream);
+      SIGB_CUDA_TRY(cudaGetLastError());
+      return SIGB_OK;
+    }
+  }
   constexpr size_t smem = 0;  // static shared memory only
   count_launch();
   timing_begin(0, stream);
