@@ -54,9 +54,9 @@ int sigb_device_sm_count(void);
 /* Kernel routing: 0 = auto (register-resident truncated kernels where an
  * instantiation exists, else fragment kernels, else level kernels),
  * 1 = level kernels only, 2 = fragment kernels (then level kernels),
- * 3 = level-slot kernels for small sparse tries (then level kernels),
  * 4 = word-set-specialised generated kernels (then fragment, level kernels).
- * Process-wide; used by the tests to check both paths against the oracle. */
+ * Process-wide; used by the tests to check both paths against the oracle.
+ * (Policy 3, the round-1 level-slot kernels, was removed and is rejected.) */
 int sigb_set_kernel_policy(int policy);
 /* Number of device kernels this library has launched (process-wide). */
 long long sigb_launch_count(void);
@@ -93,7 +93,10 @@ int sigb_wordset_tables(const uint64_t* d_codes, const int64_t* d_lengths, int64
  * reference computes missing prefixes as scratch, wordsets.py:8-9), runs
  * sigb_wordset_tables on it, and derives the kernels' schedule (parent /
  * child / level tables, partition of the trie into independent parts).
- * Holds device memory until sigb_plan_destroy.
+ * Holds device memory until sigb_plan_destroy.  The plan belongs to the device
+ * current at sigb_plan_create; every call taking the plan makes that device
+ * current for its duration (and restores the caller's), so buffers and stream
+ * must live on it.
  */
 typedef struct sigb_plan sigb_plan;
 
@@ -108,8 +111,7 @@ int64_t sigb_plan_num_parts(const sigb_plan* plan);
 int64_t sigb_plan_step_fmas(const sigb_plan* plan);
 /* Kernel family sigb_forward / sigb_backward will run for this plan under the
  * current policy: 1 = register-resident truncated kernels, 2 = register-resident
- * fragment kernels (any trie), 3 = level-slot kernels (small tries, one CTA per
- * path), 4 = word-set-specialised generated kernels (small sparse sets),
+ * fragment kernels (any trie), 4 = word-set-specialised generated kernels (small sparse sets),
  * 0 = level-synchronous trie kernels, -1 = NULL plan. */
 int sigb_plan_kernel_kind(const sigb_plan* plan);
 /* Host-only (no device): the fragment decomposition the plan would use for

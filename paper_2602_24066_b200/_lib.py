@@ -91,7 +91,7 @@ def check(rc: int) -> None:
 
 
 def set_kernel_policy(policy: int) -> None:
-    """0 auto (truncated > slot | fragment > level), 1 level only, 2 fragment first, 3 level-slot first."""
+    """0 auto (truncated > generated > fragment > level), 1 level only, 2 fragment first, 4 generated first."""
     check(lib().sigb_set_kernel_policy(int(policy)))
 
 

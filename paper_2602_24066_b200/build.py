@@ -12,8 +12,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsigkit_b200.so")
-SOURCES = ["sigb_api.cu", "sigb_plan.cu", "sigb_tables.cu", "sigb_trunc.cu", "sigb_frag.cu", "sigb_fragplan.cu", "sigb_slot.cu", "sigb_slotplan.cu", "sigb_jit.cu", "sigb_logsig.cu"]
-DEPS = SOURCES + ["sigb_internal.h", "sigb_level.cu", "sigb_trunc.cuh", "sigb_trunc_tc.cuh", "sigb_frag.cuh", "sigb_slot.cuh"]
+SOURCES = ["sigb_api.cu", "sigb_plan.cu", "sigb_tables.cu", "sigb_trunc.cu", "sigb_frag.cu", "sigb_fragplan.cu", "sigb_jit.cu", "sigb_logsig.cu"]
+DEPS = SOURCES + ["sigb_internal.h", "sigb_level.cu", "sigb_trunc.cuh", "sigb_trunc_tc.cuh", "sigb_frag.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -160,24 +160,20 @@ int backward_t(const sigb_plan* p, const void* X, int64_t B, int64_t L, const vo
 }
 
 
-// policy 0: truncated > generated (small sparse sets) > (slot | fragment) > level; 1: level only;
-// 2: fragment > level; 3: slot > level; 4: generated > fragment > level
+// policy 0: truncated > generated (small sparse sets) > fragment > level; 1: level only;
+// 2: fragment > level; 4: generated > fragment > level (3, the level-slot kernels, was removed in r02:
+// it ran at ~5% of the FMA pipe and only served sets the fragment planner cannot cut)
 bool use_trunc(const sigb_plan* p) { return g_policy == 0 && p->trunc_depth >= 2 && trunc::supported(p->d, p->trunc_depth); }
 bool use_jit(const sigb_plan* p) {
-  if (!p->jit.eligible || p->jit.broken || g_policy == 1 || g_policy == 2 || g_policy == 3) return false;
+  if (!p->jit.eligible || p->jit.broken || g_policy == 1 || g_policy == 2) return false;
   if (g_policy == 4) return true;
   if (use_trunc(p)) return false;
   // sparse sets: few words per fragment (the fragment kernels replicate chains there)
   return !p->frag.ok || (double)p->Wc / std::max(p->frag.F, 1) < 12.0;
 }
-bool use_slot(const sigb_plan* p) {
-  if (!p->slot.ok) return false;
-  if (g_policy == 3) return true;
-  return g_policy == 0 && !use_trunc(p) && !use_jit(p) && p->prefer_slot;
-}
 bool use_frag(const sigb_plan* p) {
-  if (!p->frag.ok || g_policy == 1 || g_policy == 3) return false;
-  return g_policy == 2 || (!use_trunc(p) && !use_slot(p) && !use_jit(p));
+  if (!p->frag.ok || g_policy == 1) return false;
+  return g_policy == 2 || (!use_trunc(p) && !use_jit(p));
 }
 
 int check_common(const sigb_plan* p, int dtype, int64_t B, int64_t L) {
@@ -195,12 +191,12 @@ using namespace sigb;
 
 extern "C" int sigb_version(void) { return 100; }
 extern "C" int sigb_plan_kernel_kind(const sigb_plan* plan) {
-  return plan ? (use_trunc(plan) ? 1 : use_jit(plan) ? 4 : use_slot(plan) ? 3 : use_frag(plan) ? 2 : 0) : -1;
+  return plan ? (use_trunc(plan) ? 1 : use_jit(plan) ? 4 : use_frag(plan) ? 2 : 0) : -1;
 }
 extern "C" int sigb_set_kernel_policy(int policy) {
-  if (policy < 0 || policy > 4)
-    return fail(SIGB_ERR_DOMAIN, "kernel policy must be 0 (auto), 1 (level kernels), 2 (fragment kernels), "
-                                 "3 (level-slot kernels) or 4 (generated kernels)");
+  if (policy < 0 || policy > 4 || policy == 3)
+    return fail(SIGB_ERR_DOMAIN, "kernel policy must be 0 (auto), 1 (level kernels), 2 (fragment kernels) "
+                                 "or 4 (generated kernels)");
   g_policy = policy;
   return SIGB_OK;
 }
@@ -247,6 +243,7 @@ extern "C" int sigb_forward(const sigb_plan* plan, int dtype, const void* d_X, i
                             int64_t out_ld, int64_t out_col0, int include_empty, void* d_state, void* stream) {
   int rc = check_common(plan, dtype, B, L);
   if (rc) return rc;
+  DeviceGuard guard(plan->device);
   if (include_empty && out_col0 < 1) return fail(SIGB_ERR_SHAPE, "include_empty needs out_col0 >= 1");
   if (use_trunc(plan)) {
     return trunc::forward(dtype, plan->d, plan->trunc_depth, d_X, B, L, nullptr, 1, d_out, out_ld, out_col0, include_empty,
@@ -254,10 +251,12 @@ extern "C" int sigb_forward(const sigb_plan* plan, int dtype, const void* d_X, i
   }
   if (use_jit(plan)) {
     rc = jit::forward(plan, dtype, d_X, B, L, d_out, out_ld, out_col0, include_empty, d_state, (cudaStream_t)stream);
-    if (rc == SIGB_OK || g_policy == 4) return rc;  // else: compilation failed, fall back
+    if (rc == SIGB_OK || g_policy == 4) return rc;
+    // compiling in the background (jit::kPending) or failed: the fragment kernels serve the call
+    if (plan->frag.ok)
+      return frag::forward(plan, dtype, d_X, B, L, nullptr, 1, d_out, out_ld, out_col0, include_empty, d_state,
+                           (cudaStream_t)stream);
   }
-  if (use_slot(plan))
-    return slot::forward(plan, dtype, d_X, B, L, d_out, out_ld, out_col0, include_empty, d_state, (cudaStream_t)stream);
   if (use_frag(plan))
     return frag::forward(plan, dtype, d_X, B, L, nullptr, 1, d_out, out_ld, out_col0, include_empty, d_state,
                          (cudaStream_t)stream);
@@ -272,13 +271,14 @@ extern "C" int sigb_windows(const sigb_plan* plan, int dtype, const void* d_X, i
                             const int64_t* d_bounds, int64_t K, void* d_out, void* stream) {
   int rc = check_common(plan, dtype, B, L);
   if (rc) return rc;
+  DeviceGuard guard(plan->device);
   if (K < 1 || !d_bounds) return fail(SIGB_ERR_DOMAIN, "need at least one window");
   // windows = B*K virtual paths over the same register-resident kernels as sigb_forward
   if (use_trunc(plan))
     return trunc::forward(dtype, plan->d, plan->trunc_depth, d_X, B * K, L, d_bounds, K, d_out, plan->W, 0, 0,
                           (cudaStream_t)stream);
-  // level-slot / generated kernels have no windowed form: windows run on the fragment kernels
-  if (plan->frag.ok && g_policy != 1 && g_policy != 3 && !use_trunc(plan))
+  // generated kernels have no windowed form: windows run on the fragment kernels
+  if (plan->frag.ok && g_policy != 1 && !use_trunc(plan))
     return frag::forward(plan, dtype, d_X, B * K, L, d_bounds, K, d_out, plan->W, 0, 0, nullptr, (cudaStream_t)stream);
   if (dtype == SIGB_F32)
     return forward_t<float>(plan, d_X, B, L, d_bounds, K, d_out, plan->W, 0, 0, nullptr, nullptr, 0, 0,
@@ -291,18 +291,20 @@ extern "C" int sigb_backward_workspace_size(const sigb_plan* plan, int dtype, in
                                             int64_t ckpt_stride, size_t* bytes) {
   int rc = check_common(plan, dtype, B, L);
   if (rc) return rc;
+  DeviceGuard guard(plan->device);
   if (ckpt_stride < 0) return fail(SIGB_ERR_DOMAIN, "checkpoint stride must be >= 1");
   if (B == 0 || L == 1) { *bytes = 0; return SIGB_OK; }
   if (use_trunc(plan) && ckpt_stride == 0) {
     *bytes = trunc::backward_workspace(dtype, plan->d, plan->trunc_depth, B, L);
     return SIGB_OK;
   }
-  if (use_jit(plan) && ckpt_stride == 0 && jit::ensure(const_cast<sigb_plan*>(plan), dtype, true) == SIGB_OK) {
+  if (use_jit(plan) && ckpt_stride == 0 &&
+      jit::ensure(const_cast<sigb_plan*>(plan), dtype, true, jit::wait_default()) == SIGB_OK) {
     *bytes = jit::backward_workspace(plan, dtype, B, L);
     return SIGB_OK;
   }
-  if (use_slot(plan) && ckpt_stride == 0) {
-    *bytes = slot::backward_workspace(plan, dtype, B, L);
+  if (use_jit(plan) && ckpt_stride == 0 && plan->frag.ok) {  // generated kernel still compiling
+    *bytes = frag::backward_workspace(plan, dtype, B, L);
     return SIGB_OK;
   }
   if (use_frag(plan) && ckpt_stride == 0) {
@@ -325,6 +327,7 @@ extern "C" int sigb_backward(const sigb_plan* plan, int dtype, const void* d_X, 
                              void* d_dX, void* d_dinc, void* stream) {
   int rc = check_common(plan, dtype, B, L);
   if (rc) return rc;
+  DeviceGuard guard(plan->device);
   if (ckpt_stride < 0) return fail(SIGB_ERR_DOMAIN, "checkpoint stride must be >= 1");
   if (!s_is_state && !plan->prefix_closed)
     return fail(SIGB_ERR_DOMAIN, "word set is not prefix-closed: pass the closure state from sigb_forward");
@@ -333,16 +336,18 @@ extern "C" int sigb_backward(const sigb_plan* plan, int dtype, const void* d_X, 
     return trunc::backward(dtype, plan->d, plan->trunc_depth, d_X, B, L, d_S, s_ld, s_col0, d_g, g_ld, g_col0, d_work,
                            work_bytes, d_dX, d_dinc, (cudaStream_t)stream);
   }
-  if (use_jit(plan) && ckpt_stride == 0 && B > 0 && L > 1 &&
-      jit::ensure(const_cast<sigb_plan*>(plan), dtype, true) == SIGB_OK) {
+  if (use_jit(plan) && ckpt_stride == 0 && B > 0 && L > 1) {
     if (s_is_state) { s_ld = plan->Wc; s_col0 = 0; }
-    return jit::backward(plan, dtype, d_X, B, L, d_S, s_ld, s_col0, d_g, g_ld, g_col0, d_work, work_bytes, d_dX,
-                         d_dinc, (cudaStream_t)stream);
-  }
-  if (use_slot(plan) && ckpt_stride == 0 && B > 0 && L > 1) {
-    if (s_is_state) { s_ld = plan->Wc; s_col0 = 0; }
-    return slot::backward(plan, dtype, d_X, B, L, d_S, s_ld, s_col0, d_g, g_ld, g_col0, d_work, work_bytes, d_dX,
-                          d_dinc, (cudaStream_t)stream);
+    // the generated kernel once it is loaded and the caller's workspace was sized for it (the
+    // workspace query may have run while it compiled); else the fragment kernels
+    if (jit::ensure(const_cast<sigb_plan*>(plan), dtype, true, jit::wait_default()) == SIGB_OK &&
+        work_bytes >= jit::backward_workspace(plan, dtype, B, L))
+      return jit::backward(plan, dtype, d_X, B, L, d_S, s_ld, s_col0, d_g, g_ld, g_col0, d_work, work_bytes, d_dX,
+                           d_dinc, (cudaStream_t)stream);
+    if (g_policy == 4) return fail(SIGB_ERR_DOMAIN, "backward workspace too small for the generated kernel");
+    if (plan->frag.ok)
+      return frag::backward(plan, dtype, d_X, B, L, d_S, s_ld, s_col0, d_g, g_ld, g_col0, d_work, work_bytes, d_dX,
+                            d_dinc, (cudaStream_t)stream);
   }
   if (use_frag(plan) && ckpt_stride == 0 && B > 0 && L > 1) {
     if (s_is_state) { s_ld = plan->Wc; s_col0 = 0; }

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -87,26 +89,6 @@ struct FragHost {
 // shape; false (with `why`) when no instantiation fits.
 bool plan_fragments(const Trie& t, FragHost& out, std::string& why);
 
-// Host image of a level-slot plan (sigb_slot.cuh).  Slot arrays are [KS][TPB].
-struct SlotHost {
-  int N = 0, TPB = 0;
-  int a_off = 0, t_off = 0, t_size = 0, park_off = 0, tm_off = 0, p_off = 0, p_size = 0, pstride = 0;
-  int fwd_smem = 0, bwd_smem = 0;  // elements
-  std::vector<int> tinfo, lvl, red_off, cidx, eidx;
-  std::vector<unsigned> meta0, meta1;
-  std::vector<unsigned short> pos;
-};
-bool plan_slots(const Trie& t, SlotHost& out, std::string& why);
-
-struct SlotDevPlan {
-  bool ok = false;
-  SlotHost h;  // scalars (device copies below)
-  int* tinfo = nullptr;
-  unsigned *meta0 = nullptr, *meta1 = nullptr;
-  unsigned short* pos = nullptr;
-  int *cidx = nullptr, *eidx = nullptr, *lvl = nullptr, *red_off = nullptr;
-};
-
 // Word-set-specialised (NVRTC) kernels for small tries (sigb_jit.cu).
 namespace jit {
 struct Task {
@@ -122,6 +104,7 @@ struct Cfg {
   int maxreg = 0;  // NVRTC --maxrregcount (0: launch bounds only)
   int64_t cap = 96;
 };
+struct Pending;  // a background NVRTC compile (sigb_jit.cu)
 }  // namespace jit
 struct JitHost {
   std::vector<jit::Task> fwd_tasks, bwd_tasks;
@@ -136,14 +119,20 @@ struct JitPlan {
   void* kern[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   bool failed[2][2] = {{false, false}, {false, false}};
   bool broken = false;  // some compilation failed: route this plan elsewhere
-  int* counters = nullptr;  // per-group work counters of the persistent kernels (device)
-  int ncounters = 0;
+  std::shared_ptr<jit::Pending> pending[2][2];  // background compiles in flight / finished
+  std::mutex mu;                                // guards the compile / load state above
 };
 namespace jit {
 bool eligible(const Trie& t);
 void make_plan(const Trie& t, JitHost& h);
 std::string source(const Trie& t, const JitHost& h, int dtype, bool backward);
-int ensure(sigb_plan* p, int dtype, bool backward);  // compile / load; SIGB_OK or error
+// Compile / load the generated kernel.  A cubin-cache hit loads at once; otherwise,
+// unless `wait`, the NVRTC compile runs on a background host thread and ensure
+// returns kPending (the caller serves the call with the fragment kernels) until
+// the cubin is ready.  SIGB_OK when the kernel is loaded, else an error code.
+constexpr int kPending = -1;
+int ensure(sigb_plan* p, int dtype, bool backward, bool wait);
+bool wait_default();  // policy 4 or SIGB_JIT_SYNC=1: compile synchronously
 int precompile(const Trie& t, int dtype, bool backward);  // host-only: fill the cubin cache
 int forward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, void* out, int64_t out_ld,
             int64_t out_col0, int include_empty, void* state, cudaStream_t stream);
@@ -165,6 +154,7 @@ struct FragDevPlan {
 }  // namespace sigb
 
 struct sigb_plan {
+  int device = 0;  // CUDA device current at sigb_plan_create; entry points switch to it (DeviceGuard)
   int64_t d = 0;
   int64_t W = 0;   // emitted words |I|
   int64_t Wc = 0;  // closure |cl(I)|
@@ -183,9 +173,7 @@ struct sigb_plan {
   int* d_lseg = nullptr;
   std::vector<sigb::PartDesc> h_parts;
   sigb::FragDevPlan frag;  // register-resident fragment kernels (sigb_frag.cuh), when ok
-  sigb::SlotDevPlan slot;  // level-slot kernels for small sparse tries (sigb_slot.cuh), when ok
   sigb::JitPlan jit;       // word-set-specialised kernels (sigb_jit.cu), when eligible
-  bool prefer_slot = false;  // the planner's choice between slot and fragment kernels
 
   sigb::PlanDev dev() const {
     sigb::PlanDev p;
@@ -202,6 +190,19 @@ struct sigb_plan {
 };
 
 namespace sigb {
+// Makes `dev` current for the scope and restores the caller's device: every C-ABI call
+// taking a plan launches on the plan's device whatever the calling thread has current.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
 // kernel-routing policy (sigb_set_kernel_policy) and launch counter
 extern int g_policy;
 void count_launch(int n = 1);
@@ -219,15 +220,6 @@ int backward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L,
              int64_t s_col0, const void* g, int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, void* dX,
              void* dinc, cudaStream_t stream);
 }  // namespace frag
-namespace slot {
-bool supported(int N);
-int forward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, void* out, int64_t out_ld,
-            int64_t out_col0, int include_empty, void* state, cudaStream_t stream);
-size_t backward_workspace(const sigb_plan* p, int dtype, int64_t B, int64_t L);
-int backward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, const void* S, int64_t s_ld,
-             int64_t s_col0, const void* g, int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, void* dX,
-             void* dinc, cudaStream_t stream);
-}  // namespace slot
 namespace trunc {
 bool supported(int64_t d, int depth);
 int forward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L, const int64_t* bounds, int64_t K,

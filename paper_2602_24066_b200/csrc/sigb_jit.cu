@@ -38,6 +38,9 @@
 #include <sstream>
 #include <sys/stat.h>
 
+#include <atomic>
+#include <thread>
+
 #include "sigb_internal.h"
 
 namespace sigb {
@@ -713,19 +716,30 @@ void mkdirs(const std::string& path) {
   }
 }
 
-// NVRTC -> cubin for sm_100a (cached on disk by a hash of the source).
-int compile(const std::string& src, std::string& cubin) {
+std::string cache_key(const std::string& src) {
   const char* xo = getenv("SIGB_JIT_NVRTC_OPTS");
   const std::string keysrc = xo ? src + "\n// opts: " + xo : src;
-  const std::string key = std::to_string(std::hash<std::string>{}(keysrc)) + "_" + std::to_string(src.size());
-  const std::vector<std::string> dirs = cache_dirs();
-  for (const std::string& dir : dirs) {
+  return std::to_string(std::hash<std::string>{}(keysrc)) + "_" + std::to_string(src.size());
+}
+
+// cubin from the on-disk cache, if present
+bool cache_lookup(const std::string& src, std::string& cubin) {
+  const std::string key = cache_key(src);
+  for (const std::string& dir : cache_dirs()) {
     std::ifstream in(dir + "/" + key + ".cubin", std::ios::binary);
     if (in) {
       cubin.assign(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>());
-      if (!cubin.empty()) return SIGB_OK;
+      if (!cubin.empty()) return true;
     }
   }
+  return false;
+}
+
+// NVRTC -> cubin for sm_100a (cached on disk by a hash of the source).
+int compile(const std::string& src, std::string& cubin) {
+  if (cache_lookup(src, cubin)) return SIGB_OK;
+  const std::string key = cache_key(src);
+  const std::vector<std::string> dirs = cache_dirs();
   nvrtcProgram prog;
   if (nvrtcCreateProgram(&prog, src.c_str(), "sigb_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
     return fail(SIGB_ERR_CUDA, "nvrtcCreateProgram failed");
@@ -780,17 +794,20 @@ int precompile(const Trie& t, int dtype, bool backward) {
   return compile(source(t, h, dtype, backward), cubin);
 }
 
-int ensure(sigb_plan* p, int dtype, bool backward) {
+struct Pending {
+  std::atomic<int> state{0};  // 0 compiling, 1 cubin ready, 2 failed
+  std::string cubin, err;
+};
+
+bool wait_default() {
+  static const bool sync_env = getenv("SIGB_JIT_SYNC") && atoi(getenv("SIGB_JIT_SYNC")) != 0;
+  return g_policy == 4 || sync_env;
+}
+
+namespace {
+int load(sigb_plan* p, int dtype, bool backward, const std::string& cubin) {
   JitPlan& J = p->jit;
   const int di = dtype == SIGB_F32 ? 0 : 1, bi = backward ? 1 : 0;
-  if (J.kern[di][bi]) return SIGB_OK;
-  if (J.failed[di][bi]) return fail(SIGB_ERR_UNSUPPORTED, "word-set kernel compilation failed earlier");
-  std::string cubin;
-  int rc = compile(source(J.trie, J.host, dtype, backward), cubin);
-  if (rc != SIGB_OK) {
-    J.failed[di][bi] = J.broken = true;
-    return rc;
-  }
   cudaLibrary_t lib;
   cudaKernel_t kern;
   cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
@@ -805,6 +822,46 @@ int ensure(sigb_plan* p, int dtype, bool backward) {
   J.lib[di][bi] = (void*)lib;
   J.kern[di][bi] = (void*)kern;
   return SIGB_OK;
+}
+}  // namespace
+
+int ensure(sigb_plan* p, int dtype, bool backward, bool wait) {
+  JitPlan& J = p->jit;
+  const int di = dtype == SIGB_F32 ? 0 : 1, bi = backward ? 1 : 0;
+  std::lock_guard<std::mutex> lock(J.mu);
+  if (J.kern[di][bi]) return SIGB_OK;
+  if (J.failed[di][bi]) return fail(SIGB_ERR_UNSUPPORTED, "word-set kernel compilation failed earlier");
+  std::shared_ptr<Pending>& pd = J.pending[di][bi];
+  if (!pd) {
+    const std::string src = source(J.trie, J.host, dtype, backward);
+    std::string cubin;
+    if (cache_lookup(src, cubin)) return load(p, dtype, backward, cubin);
+    pd = std::make_shared<Pending>();
+    std::shared_ptr<Pending> job = pd;
+    // host-only work (no CUDA calls): the thread owns its share of the job and may outlive the plan
+    std::thread([job, src]() {
+      std::string out;
+      const int rc = compile(src, out);
+      if (rc == SIGB_OK) {
+        job->cubin.swap(out);
+        job->state.store(1, std::memory_order_release);
+      } else {
+        job->err = "NVRTC compile of the word-set kernel failed";
+        job->state.store(2, std::memory_order_release);
+      }
+    }).detach();
+  }
+  if (wait)
+    while (pd->state.load(std::memory_order_acquire) == 0) std::this_thread::sleep_for(std::chrono::milliseconds(5));
+  const int st = pd->state.load(std::memory_order_acquire);
+  if (st == 0) return kPending;
+  if (st == 2) {
+    J.failed[di][bi] = J.broken = true;
+    return fail(SIGB_ERR_UNSUPPORTED, pd->err);
+  }
+  const int rc = load(p, dtype, backward, pd->cubin);
+  pd.reset();
+  return rc;
 }
 
 namespace {
@@ -821,16 +878,12 @@ unsigned persistent_grid(const void* kern, int threads, size_t smem, int64_t wor
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ, work_items));
 }
 
-int* counters(const sigb_plan* p, int n, cudaStream_t stream) {
-  JitPlan& J = const_cast<sigb_plan*>(p)->jit;
-  if (J.ncounters < n) {
-    if (J.counters) cudaFree(J.counters);
-    J.counters = nullptr;
-    if (cudaMalloc((void**)&J.counters, sizeof(int) * n) != cudaSuccess) return nullptr;
-    J.ncounters = n;
-  }
-  if (cudaMemsetAsync(J.counters, 0, sizeof(int) * n, stream) != cudaSuccess) return nullptr;
-  return J.counters;
+// Work counters of the persistent kernels are stream-ordered per launch (the
+// backward's live in its workspace, the forward's come from cudaMallocAsync), so
+// launches of one plan on several streams or threads never share them.
+int zero_counters(int* ctr, int n, cudaStream_t stream) {
+  SIGB_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(int) * n, stream));
+  return SIGB_OK;
 }
 
 // Bulk copies need 16-byte aligned rows: D * sizeof(R) and the base pointer.
@@ -844,14 +897,15 @@ int bulk_ok(const void* X, int dtype, int64_t d) {
 int forward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, void* out, int64_t out_ld,
             int64_t out_col0, int include_empty, void* state, cudaStream_t stream) {
   if (B == 0) return SIGB_OK;
-  int rc = ensure(const_cast<sigb_plan*>(p), dtype, false);
+  int rc = ensure(const_cast<sigb_plan*>(p), dtype, false, wait_default());
   if (rc) return rc;
   const int di = dtype == SIGB_F32 ? 0 : 1;
   const Cfg& c = cfg_of(p, dtype, false);
   int groups = (int)((p->jit.host.fwd_tasks.size() + c.warps - 1) / c.warps);
   int nblocks = (int)((B + 31) / 32);
-  int* ctr = counters(p, groups, stream);
-  if (!ctr) return fail(SIGB_ERR_CUDA, "work counters for the word-set kernel");
+  int* ctr = nullptr;
+  SIGB_CUDA_TRY(cudaMallocAsync((void**)&ctr, sizeof(int) * groups, stream));
+  if ((rc = zero_counters(ctr, groups, stream))) return rc;
   long long Bl = B, Ll = L, ld = out_ld, c0 = out_col0, Wc = p->Wc;
   int inc = include_empty, bulk = bulk_ok(X, dtype, p->d);
   void* args[] = {(void*)&X, &Bl, &Ll, &out, &ld, &c0, &inc, &state, &Wc, &nblocks, &groups, &ctr, &bulk};
@@ -860,9 +914,12 @@ int forward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, 
   count_launch();
   timing_begin(0, stream);
   const int threads = 32 * c.warps * c.pb;
-  SIGB_CUDA_TRY(cudaLaunchKernel(kern, dim3(persistent_grid(kern, threads, smem, ((int64_t)groups * nblocks + c.pb - 1) / c.pb)),
-                                 dim3(threads), args, smem, stream));
+  const cudaError_t le = cudaLaunchKernel(
+      kern, dim3(persistent_grid(kern, threads, smem, ((int64_t)groups * nblocks + c.pb - 1) / c.pb)), dim3(threads),
+      args, smem, stream);
   timing_end(0, stream);
+  SIGB_CUDA_TRY(cudaFreeAsync(ctr, stream));
+  SIGB_CUDA_TRY(le);
   return SIGB_OK;
 }
 
@@ -940,15 +997,20 @@ __global__ void __launch_bounds__(256) jit_sample_grads(const T* __restrict__ pa
 }
 }  // namespace
 
-size_t backward_workspace(const sigb_plan* p, int dtype, int64_t B, int64_t L) {
+size_t partial_bytes(const sigb_plan* p, int dtype, int64_t B, int64_t L) {
   return (dtype == SIGB_F32 ? 4 : 8) * (size_t)pad32(bwd_chunk(p, dtype, B, L)) * groups_bwd(p, dtype) *
          (size_t)(L - 1) * p->d;
+}
+
+// partials, then the persistent kernel's work counters (one int per task group)
+size_t backward_workspace(const sigb_plan* p, int dtype, int64_t B, int64_t L) {
+  return partial_bytes(p, dtype, B, L) + sizeof(int) * (size_t)groups_bwd(p, dtype);
 }
 
 int backward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, const void* S, int64_t s_ld,
              int64_t s_col0, const void* g, int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, void* dX,
              void* dinc, cudaStream_t stream) {
-  int rc = ensure(const_cast<sigb_plan*>(p), dtype, true);
+  int rc = ensure(const_cast<sigb_plan*>(p), dtype, true, wait_default());
   if (rc) return rc;
   const int di = dtype == SIGB_F32 ? 0 : 1;
   const Cfg& c = cfg_of(p, dtype, true);
@@ -956,17 +1018,20 @@ int backward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L,
   const int64_t M = L - 1, d = p->d;
   const int64_t chunk = bwd_chunk(p, dtype, B, L);
   const size_t es = dtype == SIGB_F32 ? 4 : 8;
-  if (!work || work_bytes < es * (size_t)pad32(chunk) * groups * M * d)
+  if (!work || work_bytes < backward_workspace(p, dtype, B, L))
     return fail(SIGB_ERR_DOMAIN, "backward workspace too small");
+  int* ctr = (int*)((char*)work + partial_bytes(p, dtype, B, L));
   if ((uintptr_t)work % 16) return fail(SIGB_ERR_DOMAIN, "backward workspace must be 16-byte aligned");
-  static bool attr[2] = {false, false};  // sample-grads tiles above 48 KB (fp64, large d)
-  if (!attr[di]) {
+  static bool attr[64][2] = {};  // per device: sample-grads tiles above 48 KB (fp64, large d)
+  int devno = 0;
+  cudaGetDevice(&devno);
+  if (devno >= 64 || !attr[devno][di]) {
     const int mx = (int)(es * (kTT + 1) * 32 * 33);
     SIGB_CUDA_TRY(di == 0 ? cudaFuncSetAttribute((const void*)jit_sample_grads<float>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, mx)
                           : cudaFuncSetAttribute((const void*)jit_sample_grads<double>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    attr[di] = true;
+    if (devno < 64) attr[devno][di] = true;
   }
   for (int64_t b0 = 0; b0 < B; b0 += chunk) {
     const int64_t Bc = std::min(chunk, B - b0);
@@ -978,8 +1043,7 @@ int backward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L,
     void* Sv = (void*)Sc;
     void* gv = (void*)gc;
     int grp = groups, nblocks = (int)((Bc + 31) / 32), bulk = bulk_ok(Xc, dtype, d);
-    int* ctr = counters(p, groups, stream);
-    if (!ctr) return fail(SIGB_ERR_CUDA, "work counters for the word-set kernel");
+    if ((rc = zero_counters(ctr, groups, stream))) return rc;
     void* args[] = {&Xv, &Bl, &Ll, &Sv, &sl, &s0, &gv, &gl, &g0, &work, &Bp, &nblocks, &grp, &ctr, &bulk};
     const size_t smem = smem_bytes(dtype, (int)d, c, true);
     const void* kern = (const void*)p->jit.kern[di][1];

@@ -212,6 +212,7 @@ extern "C" int sigb_plan_create(const uint64_t* codes, const int64_t* lengths, i
   split(t, {}, 0, n_roots, budget, specs);
 
   sigb_plan* plan = new sigb_plan();
+  cudaGetDevice(&plan->device);
   plan->d = d;
   plan->W = W;
   plan->Wc = Wc;
@@ -354,35 +355,6 @@ extern "C" int sigb_plan_create(const uint64_t* codes, const int64_t* lengths, i
     plan->jit.trie = t;
     jit::make_plan(t, plan->jit.host);
   }
-  // level-slot plan (sigb_slot.cuh) for small sparse tries
-  {
-    SlotHost sh;
-    std::string why;
-    if (plan_slots(t, sh, why) && slot::supported(sh.N)) {
-      SlotDevPlan& sp = plan->slot;
-      int rc3;
-      auto up = [&](auto** dst, const auto& src) -> int {
-        using E = typename std::remove_reference<decltype(src)>::type::value_type;
-        SIGB_CUDA_TRY(cudaMalloc((void**)dst, sizeof(E) * std::max<size_t>(src.size(), 1)));
-        if (!src.empty())
-          SIGB_CUDA_TRY(cudaMemcpyAsync((void*)*dst, src.data(), sizeof(E) * src.size(), cudaMemcpyHostToDevice, stream));
-        return SIGB_OK;
-      };
-      if ((rc3 = up(&sp.tinfo, sh.tinfo)) || (rc3 = up(&sp.meta0, sh.meta0)) || (rc3 = up(&sp.meta1, sh.meta1)) ||
-          (rc3 = up(&sp.pos, sh.pos)) || (rc3 = up(&sp.cidx, sh.cidx)) || (rc3 = up(&sp.eidx, sh.eidx)) ||
-          (rc3 = up(&sp.lvl, sh.lvl)) || (rc3 = up(&sp.red_off, sh.red_off))) {
-        sigb_plan_destroy(plan);
-        return rc3;
-      }
-      sp.h = sh;
-      sp.h.tinfo.clear(); sp.h.meta0.clear(); sp.h.meta1.clear(); sp.h.pos.clear();
-      sp.h.cidx.clear(); sp.h.eidx.clear();
-      sp.ok = true;
-      // measured on c3 (r01): barrier-bound at ~1.4 TF fwd vs ~11 TF for the fragment
-      // kernels, so level-slot only serves sets the fragment planner cannot cut
-      plan->prefer_slot = !plan->frag.ok;
-    }
-  }
   // perm is stored per part at node_off (same offsets as the node tables)
   auto upload = [&](auto** dst, const auto& src) -> int {
     using E = typename std::remove_reference<decltype(src)>::type::value_type;
@@ -407,6 +379,7 @@ extern "C" int sigb_plan_create(const uint64_t* codes, const int64_t* lengths, i
 
 extern "C" int sigb_plan_destroy(sigb_plan* plan) {
   if (!plan) return SIGB_OK;
+  DeviceGuard guard(plan->device);
   cudaFree(plan->d_parts);
   cudaFree(plan->d_nodeA);
   cudaFree(plan->d_nodeB);
@@ -418,9 +391,6 @@ extern "C" int sigb_plan_destroy(sigb_plan* plan) {
   cudaFree(plan->frag.sidx);
   cudaFree(plan->frag.pos);
   cudaFree(plan->frag.red_off);
-  cudaFree(plan->slot.tinfo); cudaFree(plan->slot.meta0); cudaFree(plan->slot.meta1); cudaFree(plan->slot.pos);
-  cudaFree(plan->slot.cidx); cudaFree(plan->slot.eidx); cudaFree(plan->slot.lvl); cudaFree(plan->slot.red_off);
-  cudaFree(plan->jit.counters);
   for (auto& row : plan->jit.lib)
     for (void* lib : row)
       if (lib) cudaLibraryUnload((cudaLibrary_t)lib);

@@ -97,7 +97,7 @@ class Plan:
 
     @property
     def kernel_kind(self) -> int:
-        """1 truncated, 2 fragment, 3 level-slot, 4 generated, 0 level-synchronous kernels (current policy)."""
+        """1 truncated, 2 fragment, 4 generated, 0 level-synchronous kernels (current policy)."""
         return int(_lib.lib().sigb_plan_kernel_kind(self.handle))
 
     @property

@@ -25,7 +25,7 @@ from . import _lib
 from .device import dtype_code, ptr, resolve_device, stream_ptr
 from .exceptions import DomainError, ShapeError, UnsupportedWordSetError
 from .gradient import GradBatch, backward_tensor
-from .signature import CoefficientBatch, _is_tensor, as_path_batch, forward_tensor, to_device, to_host
+from .signature import CoefficientBatch, PathBatch, _is_tensor, as_path_batch, forward_tensor, to_device, to_host
 from .wordset import WordSet, build_lyndon, build_truncated
 
 __all__ = [
@@ -71,8 +71,9 @@ def _result(ws: WordSet, full: torch.Tensor, like) -> CoefficientBatch:
 
 def _tmul(x: torch.Tensor, y: torch.Tensor, d: int, N: int, scale: float = 1.0, add0: float = 0.0) -> torch.Tensor:
     out = torch.empty_like(x)
-    _lib.check(_lib.lib().sigb_tensor_mul(dtype_code(x.dtype), ptr(x), ptr(y), x.shape[0], d, N, float(scale),
-                                          float(add0), ptr(out), stream_ptr(x.device)))
+    with torch.cuda.device(x.device):  # the ABI launches on the calling thread's current device
+        _lib.check(_lib.lib().sigb_tensor_mul(dtype_code(x.dtype), ptr(x), ptr(y), x.shape[0], d, N, float(scale),
+                                              float(add0), ptr(out), stream_ptr(x.device)))
     return out
 
 
@@ -220,9 +221,10 @@ def logsig_tensor(X: torch.Tensor, d: int, N: int) -> torch.Tensor:
     S, _ = forward_tensor(X, pr.compute)
     tb = pr.device_tables(X.device)
     out = torch.empty((X.shape[0], len(pr.lyndon)), dtype=X.dtype, device=X.device)
-    _lib.check(_lib.lib().sigb_logsig_forward(dtype_code(X.dtype), ptr(S), S.shape[0], S.shape[1],
-                                              ptr(tb["term_off"]), ptr(tb["cols"]), ptr(tb["coef"]),
-                                              out.shape[1], pr.F, ptr(out), out.shape[1], stream_ptr(X.device)))
+    with torch.cuda.device(X.device):
+        _lib.check(_lib.lib().sigb_logsig_forward(dtype_code(X.dtype), ptr(S), S.shape[0], S.shape[1],
+                                                  ptr(tb["term_off"]), ptr(tb["cols"]), ptr(tb["coef"]),
+                                                  out.shape[1], pr.F, ptr(out), out.shape[1], stream_ptr(X.device)))
     return out
 
 
@@ -245,6 +247,10 @@ def logsignature_backward(paths, d: int, N: int, grad_out, threads: int | None =
     if N < 1:
         raise DomainError(f"depth must be >= 1, got {N}")
     paths = as_path_batch(paths, dtype=np.float64)
+    if paths.dtype != np.float64:
+        # an existing PathBatch (e.g. lead_lag of float32 samples) is passed through
+        # unchanged by as_path_batch; the reference computes this backward in float64
+        paths = PathBatch(paths.samples, dtype=np.float64)
     _check(paths, d, N)
     pr = _projection(d, N)
     is_t = _is_tensor(paths.samples)
@@ -257,10 +263,13 @@ def logsignature_backward(paths, d: int, N: int, grad_out, threads: int | None =
     S, _ = forward_tensor(X, pr.compute)
     tb = pr.device_tables(dev)
     up = torch.empty_like(S)
-    _lib.check(_lib.lib().sigb_logsig_backward(
-        _lib.SIGB_F64, ptr(S), S.shape[0], S.shape[1], ptr(G), G.shape[1], ptr(tb["col_off"]),
-        ptr(tb["entries"]), ptr(tb["term_word"]), ptr(tb["cols"]), ptr(tb["coef"]), pr.F, up.shape[1], ptr(up),
-        up.shape[1], stream_ptr(dev)))
+    if not (X.dtype == S.dtype == G.dtype == up.dtype == torch.float64):
+        raise DomainError(f"log-signature backward runs in float64, got X {X.dtype}, S {S.dtype}, G {G.dtype}")
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().sigb_logsig_backward(
+            dtype_code(S.dtype), ptr(S), S.shape[0], S.shape[1], ptr(G), G.shape[1], ptr(tb["col_off"]),
+            ptr(tb["entries"]), ptr(tb["term_word"]), ptr(tb["cols"]), ptr(tb["coef"]), pr.F, up.shape[1], ptr(up),
+            up.shape[1], stream_ptr(dev)))
     dX, dinc = backward_tensor(X, pr.compute, up, 0, S=S, want_inc=True)
     if is_t:
         return GradBatch(upstream=G, increment_grads=dinc, path_grads=dX)

@@ -54,6 +54,7 @@ def test_host_only_entry_points():
     # invalid arguments fail with a code and a message, without touching a device
     assert L.sigb_set_kernel_policy(7) == 2
     assert b"policy" in L.sigb_last_error()
+    assert L.sigb_set_kernel_policy(3) == 2  # the removed level-slot family
     assert L.sigb_set_kernel_policy(0) == 0
     assert L.sigb_plan_closure_size(None) == -1
     assert L.sigb_forward(None, 0, None, 1, 2, None, 1, 0, 0, None, None) == 2

@@ -209,3 +209,20 @@ def test_batches_beyond_one_grid_row():
     dX = sk.logsignature_backward(X, 2, 2, g).path_grads
     # level-one letters: dL/dX_0 = -g, dL/dX_M = +g for the displacement part; check finite and shaped
     assert dX.shape == X.shape and np.isfinite(dX).all()
+
+
+@pytest.mark.gpu
+def test_backward_float32_path_batch_is_upcast():
+    """A float32 PathBatch (lead_lag of float32 samples) runs the float64 backward
+    like the reference (logsig.py:164-192 upcasts), bit-identical to float64 input."""
+    rng = np.random.default_rng(68)
+    X32 = (rng.random((3, 6, 2)) * 2 - 1).astype(np.float32)
+    ll32 = sk.lead_lag(X32)
+    assert ll32.dtype == np.float32
+    ll64 = sk.lead_lag(X32.astype(np.float64))
+    ly = sk.build_lyndon(4, 3)
+    g = rng.normal(size=(3, len(ly)))
+    a = sk.logsignature_backward(ll32, 4, 3, g).path_grads
+    b = sk.logsignature_backward(ll64, 4, 3, g).path_grads
+    assert a.dtype == np.float64
+    np.testing.assert_array_equal(a, b)

@@ -1,7 +1,7 @@
 """Small workload for compute-sanitizer (memcheck / racecheck / synccheck / initcheck).
 
 Runs forward, backward (fp32 autograd and fp64 drop-in) and windows through every
-kernel family (truncated, fragment, level-slot, level) on small word sets, so the sanitizer
+kernel family (truncated, fragment, generated, level) on small word sets, so the sanitizer
 sees every kernel of libsigkit_b200.so once:
 
     compute-sanitizer --tool racecheck python tools/sanitize_workload.py
