@@ -7,15 +7,24 @@ the memory-lean backward (dL/dX from S_{0,T} and a dense upstream), both
 through the C ABI (include/sigkit_b200.h) on inputs already resident in HBM.
 
 Workload (default): BASELINE.json config 5 -- truncated signature d=16,
-depth 4 (W = 69,904 words), L = 512 samples, fp32, 65,536 paths PER RANK
-(weak scaling: the batch axis shards with no collective).
-``--strong`` shards a fixed 65,536 paths instead; ``--config c2|c3|c4``
-measures another BASELINE config on the same harness.
+depth 4 (W = 69,904 words), L = 512 samples, fp32, ONE batch of 65,536 paths
+split across the ranks (strong scaling: rank r owns
+``sharding.shard_range(65536, r, N)``; the batch axis shards with no
+collective).  ``--weak`` gives every rank the config's whole batch instead;
+``--config c1|c2|c3|c4`` measures another BASELINE config on the same harness.
+
+``--gpus N`` without a torchrun environment re-launches itself under
+``torch.distributed.run`` with N ranks (one process per GPU, NCCL), so
+``python bench.py --gpus 8`` and the driver's torchrun launch are the same run.
 
 Extra keys:
   fwd          forward-only paths/s (the metric's first half)
   roofline     the dominant kernel (backward Chen kernel) against the FP32
                FMA pipe: algorithmic flop per launch / CUDA-event duration
+               (frac = frac_alg); frac_min_work credits only
+               the shared-Horner T-node FMAs the kernels must execute;
+               ncu_exec carries the executed FMA-pipe (and tensor-pipe) share
+               from the committed profiles/ capture
   roofline_fwd the same for the forward Chen kernel
   e2e          fwd+bwd paths/s through the public autograd API with the
                paths copied from pinned host memory and dL/dX + the loss
@@ -62,7 +71,8 @@ def parse_args(argv=None):
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
     p.add_argument("--config", default="c5", choices=("c1", "c2", "c3", "c4", "c5"))
     p.add_argument("--batch", type=int, default=0, help="override the per-rank batch (profiling only)")
-    p.add_argument("--strong", action="store_true", help="shard a fixed global batch instead of per-rank batches")
+    p.add_argument("--weak", action="store_true", help="every rank runs the config's whole batch (weak scaling)")
+    p.add_argument("--strong", action="store_true", help="(default) shard one fixed global batch across the ranks")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--e2e-split", type=int, default=4, help="sub-batches per e2e step (copy/compute pipeline)")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -83,29 +93,52 @@ def load_peaks() -> dict:
 
 
 def fma_peak_tflops(dtype: str, sms: int, peaks: dict) -> tuple[float, str]:
-    """FMA-pipe peak for the roofline.
+    """FMA-pipe peak for the roofline: SMs x lanes x 2 flop x clock.
 
-    MEASURED_PEAKS.json holds copy bandwidth and bf16 GEMM, not the FP32/FP64
-    FMA pipe, so the peak is MEASURED here, on this GPU, by tools/ubench_fma
-    (64 independent FFMA / 32 DFMA chains per thread, 8 CTAs per SM, best of
-    5).  If the binary is missing, fall back to SMs x lanes x 2 flop x the
-    sm_max_mhz of MEASURED_PEAKS.json, and say so.
+    MEASURED_PEAKS.json (driver-written) holds HBM copy bandwidth, bf16 GEMM and
+    the SM max clock, not an FMA-pipe figure, so the peak is the pipe width
+    times its ``sm_max_mhz`` (148 x 128 x 2 x 1965 MHz = 74.45 TF fp32,
+    37.22 TF fp64), the SM count read from the device.
     """
-    exe = os.path.join(ROOT, "tools", "ubench_fma")
-    if os.path.exists(exe):
-        try:
-            out = subprocess.run([exe, "--peak"], capture_output=True, text=True, timeout=60).stdout
-            js = json.loads(out.strip().splitlines()[-1])
-            v = js["ffma_tflops" if dtype == "fp32" else "dfma_tflops"]
-            if v > 0:
-                return v, f"measured on this GPU by tools/ubench_fma --peak ({'FFMA' if dtype == 'fp32' else 'DFMA'})"
-        except (OSError, ValueError, KeyError, IndexError, subprocess.TimeoutExpired):
-            pass
     mhz = float(peaks.get("sm_max_mhz", 1965.0))
     lanes = FP32_LANES_PER_SM if dtype == "fp32" else FP64_LANES_PER_SM
+    src = "MEASURED_PEAKS.json sm_max_mhz" if "sm_max_mhz" in peaks else "B200_PROFILING.md clocks.max.sm"
     return sms * lanes * 2 * mhz * 1e6 / 1e12, (
-        f"computed (ubench unavailable): {sms} SMs x {lanes} {dtype} FMA lanes x 2 flop x {mhz:.0f} MHz "
-        "(MEASURED_PEAKS.json sm_max_mhz)")
+        f"{sms} SMs x {lanes} {dtype} FMA lanes x 2 flop x {mhz:.0f} MHz ({src})")
+
+
+def ubench_peak_tflops(dtype: str) -> float | None:
+    """The FFMA/DFMA pipe as tools/ubench_fma --peak measures it on this GPU (context only)."""
+    exe = os.path.join(ROOT, "tools", "ubench_fma")
+    if not os.path.exists(exe):
+        return None
+    try:
+        out = subprocess.run([exe, "--peak"], capture_output=True, text=True, timeout=60).stdout
+        v = json.loads(out.strip().splitlines()[-1])["ffma_tflops" if dtype == "fp32" else "dfma_tflops"]
+        return v if v > 0 else None
+    except (OSError, ValueError, KeyError, IndexError, subprocess.TimeoutExpired):
+        return None
+
+
+def tf32_peak_tflops(peaks: dict) -> tuple[float, str]:
+    """Dense tf32 tensor peak: half the measured dense bf16 rate (the tf32:bf16 ratio of
+    B200_PROFILING.md's 1.1 / 2.25 PF), else the guide's 1.1 PF."""
+    if peaks.get("bf16_tflops"):
+        return peaks["bf16_tflops"] / 2.0, "MEASURED_PEAKS.json bf16_tflops / 2 (tf32 runs at half the bf16 rate)"
+    return 1100.0, "B200_PROFILING.md dense tf32"
+
+
+def ncu_exec(kernel: str, config: str) -> dict | None:
+    """Executed-work view of `kernel` from the committed ncu capture (profiles/ncu_summary.json)."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        ent = json.load(f).get(config, {}).get(kernel)
+    if not ent:
+        return None
+    keys = ("fma_pipe_pct", "fp64_pipe_pct", "tensor_pipe_pct", "issue_active_pct", "warps_active_pct", "source")
+    return {k: ent[k] for k in keys if ent.get(k) is not None}
 
 
 def ncu_traffic(kernel: str, config: str) -> tuple[float | None, str | None]:
@@ -122,24 +155,49 @@ def ncu_traffic(kernel: str, config: str) -> tuple[float | None, str | None]:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md).
+
+    The sampler starts before the timed region and waits for its first row, so
+    nvidia-smi's start-up does not eat a short run; ``mark()`` brackets the timed
+    region and only rows stamped inside it are summarised.
+    """
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,utilization.gpu,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, enabled: bool):
+    def __init__(self, enabled: bool, period_ms: int = 50):
         self.proc = None
+        self.t0 = self.t1 = None
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
         if enabled:
             try:
                 os.makedirs(os.path.dirname(self.path), exist_ok=True)
                 self.fh = open(self.path, "w")
                 self.proc = subprocess.Popen(
-                    ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200"],
-                    stdout=self.fh, stderr=subprocess.DEVNULL)
+                    ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms",
+                     str(period_ms)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
+                import threading
+
+                self.rows = []
+                self.first = threading.Event()
+                self.reader = threading.Thread(target=self._read, daemon=True)
+                self.reader.start()
+                self.first.wait(timeout=5.0)
             except (OSError, FileNotFoundError):
                 self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.fh.write(line)
+            self.rows.append((time.perf_counter(), line))
+            self.first.set()
+
+    def mark(self, start: bool) -> None:
+        if start:
+            self.t0 = time.perf_counter()
+        else:
+            self.t1 = time.perf_counter()
 
     def stop(self) -> dict | None:
         if self.proc is None:
@@ -149,24 +207,40 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
+        self.reader.join(timeout=2)
         self.fh.close()
         rows = []
-        with open(self.path) as f:
-            for line in f:
-                parts = [x.strip() for x in line.split(",")]
-                if len(parts) < 9:
-                    continue
-                try:
-                    rows.append((float(parts[1]), float(parts[2]), float(parts[4]), parts[5:9]))
-                except ValueError:
-                    continue
+        t0 = self.t0 if self.t0 is not None else -math.inf
+        t1 = self.t1 if self.t1 is not None else math.inf
+        for ts, line in self.rows:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9 or not t0 <= ts <= t1:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), float(parts[4]), parts[5:9]))
+            except ValueError:
+                continue
         if not rows:
-            return None
-        loaded = [r for r in rows if r[2] >= 50.0] or rows
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "note": "timed region shorter than one nvidia-smi sample; raise --steps"}
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        reasons = sorted({names[i] for r in loaded for i, v in enumerate(r[3]) if v.lower().startswith("active")})
-        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": reasons, "samples": len(loaded)}
+        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[3]) if v.lower().startswith("active")})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows),
+                "util_pct_median": statistics.median(r[2] for r in rows)}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
 
 
 def cpu_threads() -> int:
@@ -254,11 +328,13 @@ def run_reference(args) -> None:
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "paths/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * (tf + tb) / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dt,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dt,
         "data": "synthetic Brownian paths (tests/configs.py brownian)",
-        "config": {"workload": describe(args.config, cfg, ws), "per_rank_batch": cfg["B"]},
+        "config": {"workload": describe(args.config, cfg, ws), "global_batch": cfg["B"], "length": cfg["L"],
+                   "d": cfg["d"], "W": len(ws), "parallelism": "host threads (rank 0 only)"},
         "fwd": {"value": nf * args.steps / tf, "unit": "paths/s"},
-        "cpu_baseline": {"value": value, "unit": "paths/s", "cores": threads, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "paths/s", "cores": threads, "kind": "port", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "paths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -304,11 +380,11 @@ def run_ours(args) -> None:
 
     if args.batch:
         B = args.batch
-    elif args.strong:  # a fixed global batch, contiguous balanced shards (sharding.shard_range)
+    elif args.weak:  # weak scaling: every rank runs the config's batch
+        B = cfg["B"]
+    else:  # one fixed global batch, contiguous balanced shards (sharding.shard_range)
         lo, hi = shard_range(cfg["B"], rank, world)
         B = hi - lo
-    else:  # weak scaling: every rank runs the config's batch
-        B = cfg["B"]
     L, d = cfg["L"], cfg["d"]
     M = L - 1
     tdt = torch.float64 if cfg["dtype"] == np.float64 else torch.float32
@@ -357,6 +433,7 @@ def run_ours(args) -> None:
     n0 = _lib.launch_count()
     barrier()
     torch.cuda.synchronize()
+    clocks.mark(True)
     for k in range(args.steps):
         if flush is not None:
             flush.fill_(k & 0xFF)
@@ -366,6 +443,7 @@ def run_ours(args) -> None:
         plan.backward(X, S, 0, False, g, 0, 0, dXo, work=work)
         ev[3 * k + 2].record()
     torch.cuda.synchronize()
+    clocks.mark(False)
     barrier()
     launches = _lib.launch_count() - n0
     clk = clocks.stop()
@@ -379,40 +457,65 @@ def run_ours(args) -> None:
     fwd_ms = max_over_ranks(fwd_ms)
     kf_ms = max_over_ranks(kf_ms)
     kb_ms = max_over_ranks(kb_ms)
-    paths_step = cfg["B"] if (args.strong and not args.batch) else B * world
+    paths_step = B * world if (args.weak or args.batch) else cfg["B"]
     ms_per_step = total_ms / args.steps
     value = paths_step / (ms_per_step / 1e3)
     fwd_value = paths_step * args.steps / (fwd_ms / 1e3)
 
     peaks = load_peaks()
     peak, peak_src = fma_peak_tflops(dts, sms, peaks)
+    peak_ub = ubench_peak_tflops(dts)
+    tc_peak, tc_src = tf32_peak_tflops(peaks)
     f_fwd_path = 2.0 * M * sl  # one multiply-add per (word, split)
     f_bwd_path = 3.0 * f_fwd_path
+    # the least FMA work a Horner evaluation must execute: one FMA per shared (node, target
+    # length) pair per step; the backward needs at least 3 such sweeps
+    min_fwd_path = 2.0 * M * plan.step_fmas
+    min_bwd_path = 3.0 * min_fwd_path
+    tc_fwd = (plan.kernel_kind == 1 and cfg.get("kind") == "truncated" and d == 16 and cfg.get("depth") == 4
+              and tdt == torch.float32 and os.environ.get("SIGB_TRUNC_TC", "1") != "0")
 
-    def roof(kname, flop_path, k_ms, k_n, bytes_path):
+    def roof(kname, flop_path, min_path, k_ms, k_n, bytes_path):
         if k_n == 0 or k_ms <= 0:
             return None
-        achieved = flop_path * B * args.steps / (k_ms / 1e3) / 1e12  # per rank, per launch average
+        sec = k_ms / 1e3
+        achieved = flop_path * B * args.steps / sec / 1e12  # per rank, per launch average
         tr, src = ncu_traffic(kname, args.config)
         per_launch_paths = B * args.steps / k_n
-        return {"bound": "fma", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None if tr is None else tr * per_launch_paths,
-                "algorithmic_bytes": bytes_path * per_launch_paths, "flop_per_launch": flop_path * per_launch_paths,
-                "launch_ms": k_ms / k_n, "launches": k_n, "peak_source": peak_src,
-                "traffic_source": src}
+        r = {"bound": "fma", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+             "frac": achieved / peak, "frac_alg": achieved / peak,
+             "frac_min_work": min_path * B * args.steps / sec / 1e12 / peak,
+             "traffic": None if tr is None else tr * per_launch_paths,
+             "algorithmic_bytes": bytes_path * per_launch_paths, "flop_per_launch": flop_path * per_launch_paths,
+             "hbm_frac": bytes_path * B * args.steps / sec / 1e9 / float(peaks.get("hbm_gbs", 6456.8)),
+             "launch_ms": k_ms / k_n, "launches": k_n, "peak_source": peak_src, "peak_ubench": peak_ub,
+             "traffic_source": src, "ncu_exec": ncu_exec(kname, args.config)}
+        if kname == "trunc_tc_forward_kernel":
+            # leaf level on the tensor pipe: 3xTF32 (3 MMAs) x parents x d letters x 2 flop per path-step
+            leaf_parents = int((np.asarray(ws.lengths) == cfg["depth"] - 1).sum())
+            tc_flop = 3 * 2 * leaf_parents * d * M * B * args.steps / sec / 1e12
+            ffma_path = min_fwd_path - 2.0 * M * leaf_parents * d
+            t_ffma = ffma_path * B * args.steps / (peak * 1e12)
+            t_tc = 3 * 2 * leaf_parents * d * M * B * args.steps / (tc_peak * 1e12)
+            r["tensor"] = {"achieved": tc_flop, "peak": tc_peak, "unit": "TFLOP/s", "frac": tc_flop / tc_peak,
+                           "peak_source": tc_src,
+                           "note": "3xTF32 leaf update (hi.hi + hi.lo + lo.hi) executed on tcgen05"}
+            r["frac_combined"] = max(t_ffma, t_tc) / sec
+            r["combined_note"] = ("bound = max(non-leaf shared-Horner FFMA / FFMA peak, 3xTF32 leaf MMA flop / "
+                                  "tf32 peak); frac_combined = that bound / measured time")
+        return r
 
     s_el = 8 if tdt == torch.float64 else 4
     bytes_fwd = (L * d + W) * s_el
     bytes_bwd = (2 * L * d + 2 * W) * s_el
-    prefix = {1: "trunc_", 2: "frag_", 3: "slot_"}.get(plan.kernel_kind, "")
+    prefix = {1: "trunc_", 2: "frag_"}.get(plan.kernel_kind, "")
     kb_name, kf_name = prefix + "backward_kernel", prefix + "forward_kernel"
     if plan.kernel_kind == 4:
         kb_name, kf_name = "sigjit_bwd", "sigjit_fwd"
-    if (plan.kernel_kind == 1 and cfg.get("kind") == "truncated" and d == 16 and cfg.get("depth") == 4
-            and tdt == torch.float32 and os.environ.get("SIGB_TRUNC_TC", "1") != "0"):
+    if tc_fwd:
         kf_name = "trunc_tc_forward_kernel"  # leaf level on the tensor cores (csrc/sigb_trunc_tc.cuh)
-    roof_b = roof(kb_name, f_bwd_path, kb_ms, kb_n, bytes_bwd)
-    roof_f = roof(kf_name, f_fwd_path, kf_ms, kf_n, bytes_fwd)
+    roof_b = roof(kb_name, f_bwd_path, min_bwd_path, kb_ms, kb_n, bytes_bwd)
+    roof_f = roof(kf_name, f_fwd_path, min_fwd_path, kf_ms, kf_n, bytes_fwd)
     dominant = roof_b if (roof_b and kb_ms >= kf_ms) else roof_f
 
     del work
@@ -539,7 +642,7 @@ def run_ours(args) -> None:
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = cpu_threads()
         v, vf, t_f, t_b, B_f, B_b = cpu_sample(args.config, cfg, ws, threads)
-        cpu = {"value": v, "unit": "paths/s", "cores": threads, "kind": "port", "fwd_value": vf,
+        cpu = {"value": v, "unit": "paths/s", "cores": threads, "kind": "port", "fwd_value": vf, "cpu_model": cpu_model(),
                "sample": f"oracle port (oracle/sig_oracle.c, OpenMP) of the reference numba kernels: forward of "
                          f"{B_f} paths ({'f64' if tdt == torch.float64 else 'f32'}) in {t_f:.2f} s + backward of "
                          f"{B_b} paths (f64, reference contract) in {t_b:.2f} s, full L={L}"}
@@ -548,7 +651,7 @@ def run_ours(args) -> None:
         line = {
             "metric": METRIC, "value": value, "unit": "paths/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": dts.replace("fp", "f"),
+            "scaling": "weak" if (args.weak or args.batch) else "strong", "vs_baseline": None, "dtype": dts.replace("fp", "f"),
             "data": "synthetic Brownian paths on [0,1] (dX ~ N(0, 1/M)), generated on device per rank; "
                     "dense N(0,1) upstream",
             "config": {"workload": describe(args.config, cfg, ws), "per_rank_batch": B, "global_batch": paths_step,
@@ -568,12 +671,31 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
+def self_launch(args, argv) -> int:
+    """`--gpus N` outside torchrun: re-run this script as N ranks under torch.distributed.run
+    (one process per GPU, rendezvous on 127.0.0.1), the launch the driver itself uses."""
+    import socket
+
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        port = sck.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + list(argv)
+    return subprocess.run(cmd, cwd=ROOT).returncode
+
+
 def main(argv=None) -> None:
+    argv = sys.argv[1:] if argv is None else list(argv)
     args = parse_args(argv)
     if args.impl == "reference":
-        run_reference(args)
-    else:
-        run_ours(args)
+        run_reference(args)  # rank 0 alone; no process group
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(self_launch(args, argv))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus and int(os.environ.get("RANK", "0")) == 0:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; timing {world} rank(s)\n")
+    run_ours(args)
 
 
 if __name__ == "__main__":

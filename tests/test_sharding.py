@@ -105,3 +105,84 @@ def test_bench_ours_refuses_without_gpu():
     r = _bench(["--config", "c1", "--steps", "1", "--warmup", "1"])
     assert r.returncode != 0
     assert "no CPU fallback" in (r.stderr + r.stdout)
+
+
+def _nccl_worker(rank, world, port, q):
+    """One rank of the 2-GPU run: its shard of a c5-shaped batch through the public autograd
+    path, gathered back over NCCL, compared with the 1-rank result computed on cuda:0."""
+    import numpy as np
+
+    import paper_2602_24066_b200 as sk
+    from paper_2602_24066_b200.sharding import sharded_signature
+    from tests.configs import brownian
+
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world,
+                            device_id=dev)
+    try:
+        ws = sk.build_truncated(16, 4)
+        B = 37
+        X = torch.from_numpy(brownian(5, B, 64, 16).astype(np.float32))
+        g = torch.from_numpy(np.random.default_rng(105).standard_normal((B, len(ws))).astype(np.float32))
+        lo, hi = shard_range(B, rank, world)
+        Xl = X[lo:hi].to(dev).requires_grad_(True)
+        S = sharded_signature(Xl, ws)
+        S.backward(g[lo:hi].to(dev))
+        G = gather_signatures(S.detach(), B)
+        dG = gather_signatures(Xl.grad.reshape(hi - lo, -1), B)
+        ok = True
+        if rank == 0:
+            Xr = X.to(dev).requires_grad_(True)
+            S1 = sk.signature(Xr, ws)
+            S1.backward(g.to(dev))
+            ok = torch.equal(G, S1.detach()) and torch.equal(dG, Xr.grad.reshape(B, -1))
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_world2_nccl_bitwise():
+    """Two ranks over NCCL: sharded fwd+bwd with no data-path collective, then the
+    optional all-gather, bit for bit equal to the single-GPU batch (reference test_acceptance.py:332-353
+    is its only scaling gate)."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_nccl_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=600)
+    assert all(p.exitcode == 0 for p in procs)
+    res = sorted(q.get(timeout=5) for _ in range(world))
+    assert res == [(0, True), (1, True)]
+
+
+def test_bench_self_launch_command(monkeypatch):
+    """`bench.py --gpus N` outside torchrun re-runs itself under torch.distributed.run with N ranks."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    seen = {}
+
+    def fake_run(cmd, cwd=None):
+        seen["cmd"] = cmd
+
+        class R:
+            returncode = 0
+        return R()
+
+    monkeypatch.setattr(bench.subprocess, "run", fake_run)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    with pytest.raises(SystemExit) as e:
+        bench.main(["--gpus", "4", "--steps", "2"])
+    assert e.value.code == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-3:] == ["--gpus", "4", "--steps", "2"][-3:] and cmd[-4] == "--gpus"

@@ -45,7 +45,15 @@ KEYS = [
     "smsp__sass_thread_inst_executed_op_fmul_pred_on.sum",
     "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    # tcgen05 (collected with --metrics TENSOR_METRICS beside --set full)
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_tc_scope_1cta.sum",
+    "l1tex__data_pipe_tc_wavefronts_mem_shared.sum",
 ]
+# the extra --metrics list for kernels that issue tcgen05 (the names ncu --query-metrics gives on B200)
+TENSOR_METRICS = ",".join(k for k in KEYS if "tensor" in k or "_tc_" in k)
 STALL = re.compile(r"smsp__average_warps_issue_stalled_(\w+)_per_issue_active\.ratio")
 
 
@@ -94,6 +102,11 @@ def summarise(round_: str, config: str, paths: int, rep: str, js: dict) -> None:
             (1e-3 if u.get("gpu__time_duration.sum") == "us" else 1e-6 if u.get("gpu__time_duration.sum") == "ns" else 1),
             "fma_pipe_pct": num(d.get("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "nan")),
             "issue_active_pct": num(d.get("smsp__issue_active.avg.pct_of_peak_sustained_active", "nan")),
+            "warps_active_pct": num(d.get("sm__warps_active.avg.pct_of_peak_sustained_active", "nan")),
+            **({"tensor_pipe_pct": num(d["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"])}
+               if "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active" in d else {}),
+            **({"tc_pipe_pct": num(d["sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active"])}
+               if "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active" in d else {}),
             "source": f"profiles/{round_}_{base}.txt (ncu --set full, {paths} paths)",
         }
     with open(os.path.join(PROF, f"{round_}_{base}.txt"), "w") as f:
@@ -124,6 +137,9 @@ def launches(round_: str, path: str) -> None:
 
 def main(argv):
     os.makedirs(PROF, exist_ok=True)
+    if argv[0] == "--tensor-metrics":
+        print(TENSOR_METRICS)
+        return
     if argv[0] == "--launches":
         for p in argv[2:]:
             launches(argv[1], p)
