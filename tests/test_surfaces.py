@@ -134,3 +134,22 @@ def test_logsignature_and_windowed_features():
     np.testing.assert_array_equal(out[:, 6:], sk.signature_forward(X[:, 5:], ws).values)
     est = sk.WindowedSignatureFeatures(windows=[(0, 2)], depth=1).fit(np.zeros((1, 3, 2)))
     assert list(est.get_feature_names_out()) == ["0:2|1", "0:2|2"]
+
+
+@pytest.mark.gpu
+def test_features_on_cuda_tensors():
+    """The transformers also take CUDA tensors and keep the features on the device."""
+    import torch
+
+    X = random_paths(np.random.default_rng(96), 3, 9, 2)
+    Xt = torch.from_numpy(X).cuda()
+    est = sk.SignatureFeatures(depth=3).fit(Xt)
+    out = est.transform(Xt)
+    assert isinstance(out, torch.Tensor) and out.is_cuda
+    np.testing.assert_array_equal(out.cpu().numpy(), sk.SignatureFeatures(depth=3).fit(X).transform(X))
+    wt = sk.WindowedSignatureFeatures(windows=[(0, 4), (2, 9)], depth=2).fit(Xt).transform(Xt)
+    wn = sk.WindowedSignatureFeatures(windows=[(0, 4), (2, 9)], depth=2).fit(X).transform(X)
+    assert isinstance(wt, torch.Tensor)
+    assert ora.rel_err(wt.cpu().numpy(), wn) <= 1e-12
+    lt = sk.SignatureFeatures(depth=2, lead_lag=True).fit(Xt).transform(Xt)
+    np.testing.assert_array_equal(lt.cpu().numpy(), sk.SignatureFeatures(depth=2, lead_lag=True).fit(X).transform(X))
