@@ -1,4 +1,5 @@
-"""Build libsigkit_b200.so in-tree: nvcc for sm_100a, static cudart, -lineinfo.
+"""Build libsigkit_b200.so in-tree: nvcc for sm_100a, static cudart, -lineinfo; one object per
+translation unit under csrc/build/, recompiled when it or a header it includes changes.
 
     python -m paper_2602_24066_b200.build
 """
@@ -13,16 +14,20 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsigkit_b200.so")
 SOURCES = ["sigb_api.cu", "sigb_plan.cu", "sigb_tables.cu", "sigb_trunc.cu", "sigb_frag.cu", "sigb_fragplan.cu", "sigb_jit.cu", "sigb_logsig.cu"]
-DEPS = SOURCES + ["sigb_internal.h", "sigb_level.cu", "sigb_trunc.cuh", "sigb_trunc_tc.cuh", "sigb_frag.cuh"]
 
-NVCC_FLAGS = [
+COMPILE_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
+    "-Xcompiler", "-fPIC",
     "-Xptxas", "-v",
+]
+LINK_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-shared", "-cudart", "static",
     # NVRTC compiles the word-set-specialised kernels at run time (sigb_jit.cu)
     "-lnvrtc", "-Xlinker", "-rpath,/usr/local/cuda/lib64",
 ]
+OBJ = os.path.join(CSRC, "build")
 
 
 def nvcc() -> str:
@@ -32,24 +37,61 @@ def nvcc() -> str:
     return "nvcc"
 
 
+def _local_deps(src: str, seen=None) -> set[str]:
+    """The file plus every quoted #include it reaches (recursively)."""
+    import re
+
+    seen = set() if seen is None else seen
+    if src in seen or not os.path.exists(src):
+        return seen
+    seen.add(src)
+    with open(src) as f:
+        for m in re.finditer(r'^\s*#include\s+"([^"]+)"', f.read(), re.M):
+            _local_deps(os.path.normpath(os.path.join(os.path.dirname(src), m.group(1))), seen)
+    return seen
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    """nvcc each translation unit to build/*.o in parallel (only the stale ones), then link."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    os.makedirs(OBJ, exist_ok=True)
     srcs = [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
-    deps = [os.path.join(CSRC, s) for s in DEPS if os.path.exists(os.path.join(CSRC, s))]
-    deps.append(os.path.join(HERE, "..", "include", "sigkit_b200.h"))
-    if not force and os.path.exists(OUT):
-        mt = os.path.getmtime(OUT)
-        if all(os.path.getmtime(p) <= mt for p in deps):
-            return OUT
-    cmd = [nvc for nvc in [nvcc()]] + NVCC_FLAGS + ["-o", OUT] + srcs
-    res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
-    log = os.path.join(CSRC, "build.log")
-    with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError(f"nvcc failed ({res.returncode}); see {log}")
-    if verbose:
-        sys.stdout.write(res.stdout + res.stderr)
+    jobs = []
+    for s in srcs:
+        src = os.path.join(CSRC, s)
+        obj = os.path.join(OBJ, os.path.splitext(s)[0] + ".o")
+        stale = force or not os.path.exists(obj) or any(
+            os.path.getmtime(d) > os.path.getmtime(obj) for d in _local_deps(src))
+        if stale:
+            jobs.append((s, obj))
+
+    def compile_one(job):
+        s, obj = job
+        cmd = [nvcc()] + COMPILE_FLAGS + ["-c", s, "-o", obj]
+        res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+        return s, cmd, res
+
+    logs = []
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4) or 1) as ex:
+        for s, cmd, res in ex.map(compile_one, jobs):
+            logs.append(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+            if res.returncode != 0:
+                sys.stderr.write(res.stdout + res.stderr)
+                raise RuntimeError(f"nvcc failed on {s} ({res.returncode})")
+    objs = [os.path.join(OBJ, os.path.splitext(s)[0] + ".o") for s in srcs]
+    if jobs or not os.path.exists(OUT) or any(os.path.getmtime(o) > os.path.getmtime(OUT) for o in objs):
+        cmd = [nvcc()] + LINK_FLAGS + ["-o", OUT] + objs
+        res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+        logs.append(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError(f"nvcc link failed ({res.returncode})")
+    if logs:
+        with open(os.path.join(CSRC, "build.log"), "w") as f:
+            f.write("\n".join(logs))
+        if verbose:
+            sys.stdout.write("\n".join(logs))
     return OUT
 
 

@@ -92,11 +92,20 @@ int bwd(const T* X, int64_t B, int64_t L, const T* S, int64_t s_ld, int64_t s_co
   const int64_t chunk = bwd_chunk<T, D, N, G>(B, L);
   if (work_bytes < bwd_workspace<T, D, N, G>(B, L) || !work)
     return fail(SIGB_ERR_DOMAIN, "backward workspace too small");
-  constexpr size_t smem = RG::template smem_bytes<T>();
+  size_t smem = RG::template smem_bytes<T>();
   // experiment knob: SIGB_TRUNC_ASYNC=0/1 forces the staging mode (default: D >= 16)
   static const int force_async = getenv("SIGB_TRUNC_ASYNC") ? atoi(getenv("SIGB_TRUNC_ASYNC")) : -1;
   const bool async = force_async < 0 ? (D >= 16) : force_async != 0;
   auto kern = async ? trunc_backward_kernel<T, D, N, G, true> : trunc_backward_kernel<T, D, N, G, false>;
+  if constexpr (std::is_same<T, float>::value && D == 16 && N == 4 && G == 4) {
+    // leaf term on the tensor cores (TcBwd in sigb_trunc.cuh); SIGB_TRUNC_TC_BWD=0 selects the
+    // CUDA-core kernel (A/B experiments, parity tests)
+    const char* e = getenv("SIGB_TRUNC_TC_BWD");
+    if (!(e && atoi(e) == 0) && force_async != 0) {
+      kern = trunc_backward_kernel<T, D, N, G, true, true>;
+      smem += TcBwd::bytes;
+    }
+  }
   SIGB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   T* partial = (T*)work;
   for (int64_t b0 = 0; b0 < B; b0 += chunk) {

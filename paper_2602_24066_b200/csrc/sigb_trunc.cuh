@@ -24,6 +24,7 @@
 #pragma once
 
 #include "sigb_internal.h"
+#include "sigb_tc_util.cuh"
 
 namespace sigb {
 namespace trunc {
@@ -464,10 +465,30 @@ struct RedGeom {
   }
 };
 
+// Tensor-core leaf term of the backward (TC = true; fp32, D = 16, N = 4, G = 4):
+// tb[u, j] = sum_z Lambda[u z] dX_j[z] for the CTA's 1,024 leaf parents u over
+// a 32-step chunk is one (1024 x 16) . (16 x 32) product, eight tcgen05.mma
+// kind::f16 tiles of M = 128 parents, N = 32 steps, K = 16 letters.  The leaf
+// adjoints Lambda are constant over the sweep, so A is written to shared memory
+// once; B (the chunk's increments) is rebuilt per chunk.  fp32 accuracy: every A
+// row (per thread: its 4 parents) and every B column (step) is scaled by a power
+// of two into [2^13, 2^14) and split into fp16 hi + lo; D = A_hi B_hi + A_lo B_hi
+// + A_hi B_lo (3 MMAs per tile), fp32 accumulation in TMEM (7.6e-8 relative to
+// |a||b|K on rows spanning 2^+-20, tools/ubench_tc_f16.cu); the scales come off
+// exactly.  TMEM: 8 tiles x 32 steps = 256 columns, two CTAs per SM.
+struct TcBwd {
+  static constexpr int kTiles = 8;
+  static constexpr int kRows = 128;
+  static constexpr int kSteps = 32;                        // N of the MMA = the chunk
+  static constexpr int kAHalves = kTiles * kRows * 16;     // per hi / lo
+  static constexpr int kBHalves = kSteps * 16;             // per hi / lo
+  static constexpr size_t bytes = 2 * (2 * kAHalves + 2 * kBHalves) + 4 * kSteps + 16 + 1024;  // + align slack
+};
+
 // Backward.  grid: one CTA per (CTA-part of a path) -- paths [b0, b0 + nb).
 // partial layout: [(b - b0) * CPP + cip][M][D].
-template <typename T, int D, int N, int G, bool ASYNC = (D >= 16)>
-__global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
+template <typename T, int D, int N, int G, bool ASYNC = (D >= 16), bool TC = false>
+__global__ void __launch_bounds__(Cfg<D, N, G>::THREADS, TC ? 2 : 1)
     trunc_backward_kernel(const T* __restrict__ X, int64_t B, int64_t L, int64_t b0, const T* __restrict__ Sin,
                           int64_t s_ld, int64_t s_col0, const T* __restrict__ gup, int64_t g_ld, int64_t g_col0,
                           T* __restrict__ partial) {
@@ -489,6 +510,18 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
   unsigned short* key_idx = reinterpret_cast<unsigned short*>(key_off + RG::NKEY + 1);
   T* Xs2 = reinterpret_cast<T*>(
       smem_raw + ((((size_t)(reinterpret_cast<unsigned char*>(key_idx + RG::NE) - smem_raw)) + 15) & ~size_t(15)));
+  static_assert(!TC || (sizeof(T) == 4 && D == 16 && N == 4 && G == 4 && C::CPP == 4 && ASYNC && RG::CH == 32),
+                "tensor-core leaf term: fp32, d = 16, depth 4, four CTAs of 1,024 leaf parents per path");
+  // TC region (after the second sample buffer): A hi/lo, B hi/lo (fp16), 1/sigma per step, mbarrier, TMEM slot
+  __half* Ah = reinterpret_cast<__half*>(
+      smem_raw + ((((size_t)(reinterpret_cast<unsigned char*>(Xs2 + C::PPC * (RG::CH + 1) * D) - smem_raw)) + 1023) &
+                  ~size_t(1023)));
+  __half* Al = Ah + TcBwd::kAHalves;
+  __half* Bh = Al + TcBwd::kAHalves;
+  __half* Bl = Bh + TcBwd::kBHalves;
+  float* inv_sig = reinterpret_cast<float*>(Bl + TcBwd::kBHalves);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(inv_sig + TcBwd::kSteps);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 1);
   const int64_t cta = blockIdx.x + (C::CPP > 1 ? b0 * C::CPP : b0 / C::PPC);
   const Frag<D, N, G> f(cta, threadIdx.x);
   const int64_t b_first = C::CPP > 1 ? f.b : cta * C::PPC;
@@ -544,6 +577,39 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
       key_idx[fill[key_of(e)]++] = (unsigned short)((wr * RG::CH * RG::GPW + gg) * NCc + k);
     }
   }
+  // TC: TMEM, the mbarrier and the A operand (this thread's 4 rows: tiles mt0 + g, row = its TMEM lane)
+  uint32_t tmem = 0, mma_phase = 0;
+  float inv_s = 1.f;
+  const int mt0 = (warp >> 2) * G;
+  const uint32_t lane_addr = (uint32_t)(32 * (warp & 3)) << 16;
+  if constexpr (TC) {
+    if (warp == 0) tcu::tmem_alloc<256>(tmem_slot);
+    if (threadIdx.x == 32) tcu::mbar_init(mbar, 1);
+    float amax = 0.f;
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int z = 0; z < D; ++z) amax = fmaxf(amax, fabsf(lam.leaf[g][z]));
+    const float sc = tcu::pow2_scale(amax);
+    inv_s = 1.f / sc;  // exact: a power of two
+    const int r = 32 * (warp & 3) + lane;
+    const T* grow = gup + (live ? f.b : 0) * g_ld + g_col0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+      for (int kg = 0; kg < 2; ++kg) {
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = live ? grow[f.leaf_index(g, 8 * kg + i)] : 0.f;
+        const int off = (mt0 + g) * TcBwd::kRows * 16 + tcu::kmajor_off16<2>(r, 8 * kg);
+        tcu::split8_store(v, sc, Ah + off, Al + off);
+      }
+    }
+    tcu::fence_before();
+    __syncthreads();
+    tcu::fence_after();
+    tmem = *tmem_slot;
+  }
   const int nchunks = (int)((M + RG::CH - 1) / RG::CH);
   // ASYNC: double-buffered cp.async staging of chunk c-1 while chunk c computes
   if (ASYNC && nchunks > 0)
@@ -563,6 +629,49 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
       }
       __syncthreads();
       if (c > 0) issue_samples<T, D, C::PPC, RG::CH>(X, b_first, B, L, j0 - RG::CH, RG::CH, Xb == Xs ? Xs2 : Xs);
+      if constexpr (TC) {
+        // B operand: one thread per step row (rows past the chunk are zero), scaled per step
+        if (threadIdx.x < TcBwd::kSteps) {
+          const int sr = threadIdx.x;
+          float v[16];
+#pragma unroll
+          for (int z = 0; z < 16; ++z) v[z] = sr < cs ? Dl[sr * D + z] : 0.f;
+          float amax = 0.f;
+#pragma unroll
+          for (int z = 0; z < 16; ++z) amax = fmaxf(amax, fabsf(v[z]));
+          const float sc = tcu::pow2_scale(amax);
+          inv_sig[sr] = 1.f / sc;
+#pragma unroll
+          for (int kg = 0; kg < 2; ++kg) {
+            float w[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[i] = v[8 * kg + i];
+            const int off = tcu::kmajor_off16<2>(sr, 8 * kg);
+            tcu::split8_store(w, sc, Bh + off, Bl + off);
+          }
+        }
+        tcu::fence_async_smem();  // generic-proxy writes of A / B -> the tensor core's async proxy
+        tcu::fence_before();      // the previous chunk's tcgen05.ld before the MMAs overwrite D
+        __syncthreads();
+        tcu::fence_after();
+        if (warp == 0) {
+          constexpr uint32_t id = tcu::idesc_f16(128, TcBwd::kSteps);
+          const uint64_t bh = tcu::smem_desc(tcu::su32(Bh), 128, 256), bl = tcu::smem_desc(tcu::su32(Bl), 128, 256);
+#pragma unroll
+          for (int mt = 0; mt < TcBwd::kTiles; ++mt) {
+            const uint64_t ah = tcu::smem_desc(tcu::su32(Ah + mt * TcBwd::kRows * 16), 128, 256);
+            const uint64_t al = tcu::smem_desc(tcu::su32(Al + mt * TcBwd::kRows * 16), 128, 256);
+            const uint32_t d = tmem + TcBwd::kSteps * mt;
+            tcu::mma_ss_f16(d, ah, bh, id, 0u);  // A_hi B_hi
+            tcu::mma_ss_f16(d, al, bh, id, 1u);  // A_lo B_hi
+            tcu::mma_ss_f16(d, ah, bl, id, 1u);  // A_hi B_lo
+          }
+          tcu::mma_commit(mbar);
+        }
+        tcu::mbar_wait(mbar, mma_phase);
+        mma_phase ^= 1u;
+        tcu::fence_after();
+      }
     } else {
       stage_increments<T, D, C::PPC, RG::CH>(X, b_first, B, L, j0, cs, Xs, Dl);
     }
@@ -574,8 +683,16 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
     for (int s = cs - 1; s >= 0; --s) {
       StepIncr<T, D, N, G> in;
       // (a) rebuild S_{0,t_j} = S_{0,t_{j+1}} ⊗ exp(-dX_j) (chain and mids only)
-      in.load(rows + s * D, f, T(-1));
-      if constexpr (PERM) {  // leaf increments in the lane's permuted letter order (quad-level XOR)
+      if constexpr (TC) {  // the leaf letters' increments only feed the MMA: mid and chain letters here
+        const T* row = rows + s * D;
+        const float4 y = *reinterpret_cast<const float4*>(row + f.q * G);
+        in.dy[0] = -y.x; in.dy[1] = -y.y; in.dy[2] = -y.z; in.dy[3] = -y.w;
+#pragma unroll
+        for (int k = 0; k < NC; ++k) in.dc[k] = -row[f.chain_letter[k]];
+      } else {
+        in.load(rows + s * D, f, T(-1));
+      }
+      if constexpr (PERM && !TC) {  // leaf increments in the lane's permuted letter order (quad-level XOR)
         const T* row = rows + s * D;
 #pragma unroll
         for (int k = 0; k < D / 4; ++k) {
@@ -585,8 +702,10 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
       }
       chen_step<T, D, N, G, false>(st, in);
       // (b) forward partials from S_{0,t_j}
+      if constexpr (!TC) {
 #pragma unroll
-      for (int i = 0; i < D; ++i) in.dz[i] = -in.dz[i];
+        for (int i = 0; i < D; ++i) in.dz[i] = -in.dz[i];
+      }
 #pragma unroll
       for (int g = 0; g < G; ++g) in.dy[g] = -in.dy[g];
 #pragma unroll
@@ -601,11 +720,31 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
       for (int z = 0; z < D; ++z) gl[z] = T(0);
       T gm[G];
       T tbp1 = T(0), tbp2 = T(0);  // Tbar(gp, N-1), Tbar(gp, N) from the mids
+      T tbv[G];  // TC: Tbar(u_g, N) = sum_z Lambda[u_g z] dX[z], from the chunk's MMAs
+      if constexpr (TC) {
+        const float kf = inv_s * inv_sig[s];
+        uint32_t rr[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) rr[g] = tcu::tmem_ld1(tmem + lane_addr + TcBwd::kSteps * (mt0 + g) + s);
+        tcu::tmem_ld_wait();
+#pragma unroll
+        for (int g = 0; g < G; ++g) tbv[g] = __uint_as_float(rr[g]) * kf;
+      }
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const T tm = fma(in.dy[g] * inv<T, 2>(), tN, st.mid[g]);  // T(u_g, N)
         T tb0 = T(0), tb1 = T(0);
-        if constexpr (sizeof(T) == 4 && D % 2 == 0) {
+        if constexpr (TC) {
+          const float2 tm2 = make_float2(tm, tm);
+#pragma unroll
+          for (int z = 0; z < D; z += 2) {
+            const float2 r = __ffma2_rn(make_float2(lam.leaf[g][z], lam.leaf[g][z + 1]), tm2,
+                                        make_float2(gl[z], gl[z + 1]));
+            gl[z] = r.x;
+            gl[z + 1] = r.y;
+          }
+          tb0 = tbv[g];
+        } else if constexpr (sizeof(T) == 4 && D % 2 == 0) {
           // packed f32x2: even/odd letters in the two halves (as the scalar split)
           float2 tb2 = make_float2(0.f, 0.f);
           const float2 tm2 = make_float2(tm, tm);
@@ -630,7 +769,7 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
             }
           }
         }
-        const T tb = tb0 + tb1;  // Tbar(u_g, N)
+        const T tb = TC ? tb0 : tb0 + tb1;  // Tbar(u_g, N)
         const T lm = lam.mid[g];  // Tbar(u_g, N-1)
         tbp1 = fma(in.dy[g], lm, tbp1);
         tbp2 = fma(in.dy[g] * inv<T, 2>(), tb, tbp2);
@@ -733,6 +872,11 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
       partial[(((b - b0) * C::CPP + f.cip) * M + j0 + s) * D + z] = acc;
     }
     __syncthreads();
+  }
+  if constexpr (TC) {
+    tcu::fence_before();
+    __syncthreads();
+    if (warp == 0) tcu::tmem_dealloc<256>(tmem);
   }
 }
 

@@ -23,6 +23,7 @@
 // [16 mt, 16 mt + 16); A tile mt at 128 + 16 mt (+8 for the lo part).
 #pragma once
 
+#include "sigb_tc_util.cuh"
 #include "sigb_trunc.cuh"
 
 namespace sigb {
@@ -36,62 +37,24 @@ constexpr int kTmemCols = 256;
 constexpr int kACol = 128;
 constexpr int kChunkTc = 32;  // steps of samples staged per round
 
-__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+using tcu::bar_arrive;
+using tcu::bar_sync;
+using tcu::idesc_tf32;
+using tcu::mbar_wait;
+using tcu::mma_commit;
+using tcu::smem_desc;
+using tcu::su32;
 
 // high part of the 3xTF32 split: the top 19 bits (truncation; one LOP3 -- cvt.rna.tf32
 // is emulated with ~8 integer instructions on sm_100a).  x - hi is exact, and the
 // MMA's own truncation of lo costs < 2^-20 |x|.
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
-// canonical K-major no-swizzle shared-memory operand descriptor (sm_100)
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
-  return (uint64_t)((addr >> 4) & 0x3fff) | ((uint64_t)((lbo >> 4) & 0x3fff) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | ((uint64_t)1 << 46);
-}
-
-// instruction descriptor: D f32, A/B tf32, both K-major
-__host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
-}
-
-// A from TMEM, B from shared memory; issued by the warp, one elected lane runs it
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
-      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc));
+  tcu::mma_ts_tf32(d, a, bdesc, idesc, acc);
 }
 
-__device__ __forceinline__ void mma_commit(uint64_t* mbar) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(su32(mbar))
-      : "memory");
-}
-
-// bounded wait: a lost arrival traps (the launch fails) instead of hanging the GPU
-__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
-  const uint32_t a = su32(mbar);
-  for (uint32_t it = 0;; ++it) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-    if (ok) return;
-    if (it > (1u << 26)) __trap();
-  }
-}
-
-__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void bar_arrive(int id, int n) {
-  asm volatile("barrier.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-__device__ __forceinline__ int kmajor_off(int row, int k) {  // rows x 8 steps, core matrices [row/8][k/4]
-  return ((row >> 3) * 2 + (k >> 2)) * 32 + (row & 7) * 4 + (k & 3);
-}
+__device__ __forceinline__ int kmajor_off(int row, int k) { return tcu::kmajor_off32<2>(row, k); }  // rows x 8 steps
 
 template <int D, int N>
 __global__ void __launch_bounds__(kThreadsTc, 2)

@@ -54,3 +54,59 @@ def test_tc_forward_deterministic(monkeypatch):
     a = sk.signature(X, ws)
     b = sk.signature(X, ws)
     assert torch.equal(a, b)
+
+
+# -- backward: the leaf term tb = Lambda . dX on the tensor cores (TcBwd, sigb_trunc.cuh) ----------
+
+
+def _autograd(X, ws, g, tc_bwd, monkeypatch):
+    monkeypatch.setenv("SIGB_TRUNC_TC_BWD", "1" if tc_bwd else "0")
+    Xt = torch.from_numpy(X).cuda().requires_grad_(True)
+    S = sk.signature(Xt, ws)
+    S.backward(torch.from_numpy(g).cuda())
+    return Xt.grad.cpu().numpy()
+
+
+@pytest.mark.parametrize("L", [2, 3, 17, 33, 34, 65, 200])
+def test_tc_backward_matches_oracle(L, monkeypatch):
+    """Chunk edges (M < 32, M = 32, M = 33, ragged last chunk) against the fp64 oracle and the
+    CUDA-core backward."""
+    ws = sk.build_truncated(16, 4)
+    B = 3
+    X = brownian(40 + L, B, L, 16).astype(np.float32)
+    g = np.random.default_rng(L).standard_normal((B, len(ws))).astype(np.float32)
+    dX = _autograd(X, ws, g, True, monkeypatch)
+    _, dref = ora.backward(X.astype(np.float64), ws.codes, ws.lengths, 16, g.astype(np.float64))
+    assert ora.rel_err(dX, dref) <= TOL32
+    assert ora.rel_err(dX, _autograd(X, ws, g, False, monkeypatch)) <= TOL32
+
+
+def test_tc_backward_scaled_inputs(monkeypatch):
+    """Power-of-two operand scaling: upstream rows spanning 2^-30..2^30, a path scaled by 1e4,
+    one by 1e-4, a constant stretch (zero increments), a zero upstream path."""
+    ws = sk.build_truncated(16, 4)
+    B, L = 5, 70
+    X = brownian(77, B, L, 16)
+    X[1] *= 1e4
+    X[2] *= 1e-4
+    X[3, 20:40] = X[3, 20]
+    X = X.astype(np.float32)
+    rng = np.random.default_rng(78)
+    g = rng.standard_normal((B, len(ws)))
+    g *= np.exp2(rng.integers(-30, 31, size=(B, len(ws))))
+    g[4] = 0.0
+    g = g.astype(np.float32)
+    dX = _autograd(X, ws, g, True, monkeypatch)
+    _, dref = ora.backward(X.astype(np.float64), ws.codes, ws.lengths, 16, g.astype(np.float64))
+    for b in range(B):
+        assert ora.rel_err(dX[b], dref[b]) <= TOL32, b
+    assert not np.any(dX[4])
+
+
+def test_tc_backward_deterministic(monkeypatch):
+    ws = sk.build_truncated(16, 4)
+    X = brownian(81, 9, 100, 16).astype(np.float32)
+    g = np.random.default_rng(82).standard_normal((9, len(ws))).astype(np.float32)
+    a = _autograd(X, ws, g, True, monkeypatch)
+    b = _autograd(X, ws, g, True, monkeypatch)
+    assert np.array_equal(a, b)
