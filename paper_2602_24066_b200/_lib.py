@@ -14,6 +14,9 @@ from . import exceptions as E
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsigkit_b200.so")
+# developer override (ablation / A-B builds under tools/); the product path is LIB_PATH
+if os.environ.get("SIGB_LIB_PATH"):
+    LIB_PATH = os.environ["SIGB_LIB_PATH"]
 
 SIGB_OK = 0
 SIGB_F32 = 0

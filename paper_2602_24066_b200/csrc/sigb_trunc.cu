@@ -8,6 +8,7 @@
 
 #include "sigb_trunc.cuh"
 #include "sigb_trunc_tc.cuh"
+#include "sigb_trunc_pq.cuh"
 
 namespace sigb {
 namespace trunc {
@@ -97,23 +98,39 @@ int bwd(const T* X, int64_t B, int64_t L, const T* S, int64_t s_ld, int64_t s_co
   static const int force_async = getenv("SIGB_TRUNC_ASYNC") ? atoi(getenv("SIGB_TRUNC_ASYNC")) : -1;
   const bool async = force_async < 0 ? (D >= 16) : force_async != 0;
   auto kern = async ? trunc_backward_kernel<T, D, N, G, true> : trunc_backward_kernel<T, D, N, G, false>;
+  bool pq_kernel = false;
   if constexpr (std::is_same<T, float>::value && D == 16 && N == 4 && G == 4) {
-    // leaf term on the tensor cores (TcBwd in sigb_trunc.cuh); SIGB_TRUNC_TC_BWD=0 selects the
-    // CUDA-core kernel (A/B experiments, parity tests)
+    // leaf level on the tensor cores.  SIGB_TRUNC_TC_BWD selects: 2 (default) the P/Q kernel
+    // (sigb_trunc_pq.cuh, both leaf sums on tcgen05), 1 the parent pull-back only on tcgen05
+    // (TcBwd), 0 the CUDA-core kernel (A/B experiments, parity tests)
     const char* e = getenv("SIGB_TRUNC_TC_BWD");
-    if (!(e && atoi(e) == 0) && force_async != 0) {
+    const int mode = e ? atoi(e) : 2;
+    if (mode == 2 && force_async != 0) {
+      pq_kernel = true;
+      smem = pq::kSmem;
+      SIGB_CUDA_TRY(cudaFuncSetAttribute(pq::trunc_pq_backward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+    } else if (mode == 1 && force_async != 0) {
       kern = trunc_backward_kernel<T, D, N, G, true, true>;
       smem += TcBwd::bytes;
     }
   }
-  SIGB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (!pq_kernel) SIGB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   T* partial = (T*)work;
   for (int64_t b0 = 0; b0 < B; b0 += chunk) {
     const int64_t Bc = std::min(chunk, B - b0);
     const int64_t grid = C::CPP > 1 ? Bc * C::CPP : (Bc + C::PPC - 1) / C::PPC;
     count_launch(2);
     timing_begin(1, stream);
-    kern<<<(unsigned)grid, C::THREADS, smem, stream>>>(X, B, L, b0, S, s_ld, s_col0, g, g_ld, g_col0, partial);
+    if constexpr (std::is_same<T, float>::value && D == 16 && N == 4 && G == 4) {
+      if (pq_kernel)
+        pq::trunc_pq_backward_kernel<<<(unsigned)grid, pq::kBlock, smem, stream>>>(X, B, L, b0, S, s_ld, s_col0, g,
+                                                                                     g_ld, g_col0, partial);
+      else
+        kern<<<(unsigned)grid, C::THREADS, smem, stream>>>(X, B, L, b0, S, s_ld, s_col0, g, g_ld, g_col0, partial);
+    } else {
+      kern<<<(unsigned)grid, C::THREADS, smem, stream>>>(X, B, L, b0, S, s_ld, s_col0, g, g_ld, g_col0, partial);
+    }
     timing_end(1, stream);
     SIGB_CUDA_TRY(cudaGetLastError());
     const int64_t n = Bc * L * D;

@@ -1,0 +1,437 @@
+// Truncated backward for d = 16, depth 4, fp32 (config 5) with the whole leaf
+// level on the tensor cores: the "P/Q" form.
+//
+// The leaves (words gp.y.z of length 4; gp a length-2 grand-parent, y the
+// parent's last letter, z the leaf letter) carry constant adjoints
+// Lambda[gp, y, z] (the upstream gradient; a leaf is a single Horner node).  They
+// enter the reverse sweep twice per step j (_kernels.py:152-173):
+//   (1) the pull-back to their parent u = gp.y:   tb[u]   = sum_z Lambda[gp,y,z] dX_j[z]
+//   (2) the gradient of letter z:                 gl[gp,z] = sum_y Lambda[gp,y,z] T(gp.y, 4)_j
+// with T(gp.y, 4)_j = S_j(gp.y) + dX_j[y]/2 T(gp, 4)_j the parent's Horner partial.
+// On CUDA cores both are 16-term sums per (word, step): 2 x 65,536 FMAs per
+// path-step plus a 16-letter butterfly per thread-step (round 1's kernel).
+//
+// (1) is a (1024 x 16) . (16 x 32-step) product per CTA and chunk -- D1 on tcgen05.
+// (2) splits by linearity into
+//   gl[gp,z] = P_j[gp,z] + T(gp,4)_j / 2 * Q_j[gp,z],
+//   Q_j[gp,z] = sum_y Lambda[gp,y,z] dX_j[y]            (the transposed product -- D2 on tcgen05)
+//   P_j[gp,z] = sum_y Lambda[gp,y,z] S_j(gp.y)          (kept as state: one FMA per step)
+// because the memory-lean reconstruction S_j(gp.y) = S_{j+1}(gp.y) - dX_j[y] Tr(gp, 3)_j
+// (Tr: the partial of the exp(-dX) step) gives P_j = P_{j+1} - Tr(gp,3)_j Q_j.
+// So the CUDA cores keep two FMAs per (grand-parent, letter) and step for the
+// leaves instead of 32, no 64-register Lambda block, and a 4-letter reduction
+// per thread instead of 16.
+//
+// Tensor-core operands (kind::f16, M = 128 rows, N = 16 steps, K = 16 letters):
+// A1 rows = parents u (K = z), A2 rows = (gp, z) pairs (K = y), both constant
+// over the sweep and written to shared memory once; B = the chunk's increments
+// (K = letter, N = step), rebuilt per chunk.  fp32 accuracy from a scaled 3-pass
+// fp16 split (A rows per thread and B columns per step scaled by powers of two
+// into [2^13, 2^14), x = hi + lo, D = A_hi B_hi + A_lo B_hi + A_hi B_lo;
+// tools/ubench_tc_f16.cu: 7.6e-8 relative).  Steps 16-31 and 0-15 of a chunk
+// are two MMA groups with their own mbarrier, so the second group runs while
+// the sweep walks the first.  TMEM: {D1, D2} x 8 tiles x 16 steps x 2 groups =
+// 512 columns; one CTA (a quarter path: 64 grand-parents x 4 letter quads) per
+// SM (152 KB shared memory).
+//
+// Thread (grand-parent gp, quad q) owns: the chain of gp (levels 1-2, computed
+// redundantly by the quad), parents gp.y for y in 4q..4q+3 (state, adjoint, D1
+// rows) and pairs (gp, z) for z in 4q..4q+3 (P state, D2 rows).  Its letter sums
+// for the quad's four letters (parent terms + leaf terms + chain terms) are
+// reduced over the warp's 8 grand-parents by a 4-shuffle transposing butterfly,
+// parked per warp in shared memory, and summed over the 8 warps in fixed order
+// per chunk into the partial buffer trunc_sample_grads telescopes.
+#pragma once
+
+#include "sigb_tc_util.cuh"
+#include "sigb_trunc.cuh"
+
+namespace sigb {
+namespace trunc {
+namespace pq {
+
+constexpr int D = 16;
+constexpr int kThreads = 256;  // compute threads: a quarter path
+constexpr int kBlock = kThreads + 32;  // + the producer warp
+constexpr int CPP = 4;         // CTAs per path
+constexpr int CH = 32;         // steps per chunk
+constexpr int NG = 16;         // steps per MMA group (MMA N)
+constexpr int kTiles = 8;      // 1,024 rows per operand / 128
+constexpr int kRowHalves = 128 * 16;
+constexpr int kAHalves = kTiles * kRowHalves;
+
+// shared memory (bytes); B, increments, parked sums and 1/sigma are double-buffered by chunk parity
+constexpr int oA1h = 0, oA1l = oA1h + 2 * kAHalves, oA2h = oA1l + 2 * kAHalves, oA2l = oA2h + 2 * kAHalves;
+constexpr int kBBytes = 2 * CH * 16;                   // one of hi / lo
+constexpr int oB = oA2l + 2 * kAHalves;                // [2 buffers][hi, lo]
+constexpr int oXs = oB + 2 * 2 * kBBytes;              // two sample buffers (CH + 1) x D
+constexpr int oDl = oXs + 2 * 4 * (CH + 1) * D;        // [2][CH][D] increments
+constexpr int oRed = oDl + 2 * 4 * CH * D;             // [2][8 warps][CH][D] per-warp letter sums
+constexpr int oSig = oRed + 2 * 4 * 8 * CH * D;        // [2][CH] 1 / sigma per step
+constexpr int oBar = oSig + 2 * 4 * CH;                // mbarriers: MMA group 0, 1; increments ready 0, 1
+constexpr int oSlot = oBar + 32;
+constexpr size_t kSmem = oSlot + 16;
+
+// canonical word indices of a full truncation d = 16: levels start at 0, 16, 272, 4368
+__device__ __forceinline__ int idx2(int gp) { return 16 + gp; }
+__device__ __forceinline__ int idx3(int gp, int y) { return 272 + gp * 16 + y; }
+__device__ __forceinline__ int idx4(int gp, int y, int z) { return 4368 + (gp * 16 + y) * 16 + z; }
+
+__device__ __forceinline__ void ld_wait8(uint32_t (&r)[8]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7])
+               :
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kBlock, 1)
+    trunc_pq_backward_kernel(const float* __restrict__ X, int64_t B, int64_t L, int64_t b0,
+                             const float* __restrict__ Sin, int64_t s_ld, int64_t s_col0,
+                             const float* __restrict__ gup, int64_t g_ld, int64_t g_col0,
+                             float* __restrict__ partial) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __half* A1h = reinterpret_cast<__half*>(sm + oA1h);
+  __half* A1l = reinterpret_cast<__half*>(sm + oA1l);
+  __half* A2h = reinterpret_cast<__half*>(sm + oA2h);
+  __half* A2l = reinterpret_cast<__half*>(sm + oA2l);
+  auto Bhi = [&](int db) { return reinterpret_cast<__half*>(sm + oB + db * 2 * kBBytes); };
+  auto Blo = [&](int db) { return reinterpret_cast<__half*>(sm + oB + db * 2 * kBBytes + kBBytes); };
+  auto Xsb = [&](int db) { return reinterpret_cast<float*>(sm + oXs) + db * (CH + 1) * D; };
+  auto Dlb = [&](int db) { return reinterpret_cast<float*>(sm + oDl) + db * CH * D; };
+  float(*red)[8][CH][D] = reinterpret_cast<float(*)[8][CH][D]>(sm + oRed);
+  auto isig = [&](int db) { return reinterpret_cast<float*>(sm + oSig) + db * CH; };
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + oBar);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(sm + oSlot);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool producer = warp == kThreads / 32;
+  const int64_t b = b0 + blockIdx.x / CPP;  // the grid covers live paths only
+  const int cip = blockIdx.x % CPP;
+  const int q = lane & 3;
+  const int gp = ((cip * kThreads + tid) >> 2) & 255;  // 0..255 (the producer warp's value is unused)
+  const int la = gp >> 4, lb = gp & 15;       // letters of the chain: node la (level 1), node gp (level 2)
+  const int64_t M = L - 1;
+  const int r = 32 * (warp & 3) + lane;       // this thread's row in every tile = its TMEM lane
+  const int mt0 = (warp >> 2) * 4;            // its tiles mt0 .. mt0 + 3
+  const uint32_t lane_addr = (uint32_t)(32 * (warp & 3)) << 16;
+
+  if (producer) {
+    tcu::tmem_alloc<512>(slot);
+    if (lane == 0) {
+      tcu::mbar_init(&mbar[0], 1);  // MMA groups: one tcgen05.commit each per chunk
+      tcu::mbar_init(&mbar[1], 1);
+      tcu::mbar_init(&mbar[2], 32);  // increments / B of buffer 0, 1 ready: the producer's 32 lanes
+      tcu::mbar_init(&mbar[3], 32);
+    }
+  }
+
+  // ---- terminal state, adjoint seeds, P, and the constant A operands ----
+  // The CTA's 16,384 leaf adjoints (contiguous in the upstream row: leaves of grand-parents
+  // 64 cip .. 64 cip + 63) and 1,024 parent values are staged in shared memory first (all 288
+  // threads, coalesced cp.async; the A2 region and the parked-sums region are free until the
+  // sweep), so each thread reads its A1 rows / A2 columns / P terms from shared memory.
+  const float* srow = Sin + b * s_ld + s_col0;
+  const float* grow = gup + b * g_ld + g_col0;
+  float* lstage = reinterpret_cast<float*>(sm + oA2h);  // [64 gp][16 y][16 z] fp32 (64 KB = A2 hi + lo)
+  float* sstage = reinterpret_cast<float*>(sm + oRed);  // [64 gp][16 y] parent values
+  {
+    const float* lsrc = grow + idx4(64 * cip, 0, 0);
+    for (int i = tid; i < 64 * 256; i += kBlock)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tcu::su32(lstage + i)), "l"(lsrc + i) : "memory");
+    const float* ssrc = srow + idx3(64 * cip, 0);
+    for (int i = tid; i < 64 * 16; i += kBlock)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tcu::su32(sstage + i)), "l"(ssrc + i) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  float sc0 = srow[la], sc1 = srow[idx2(gp)];
+  float lc0 = (q == 0 && lb == 0) ? grow[la] : 0.f;  // seeded once per chain node
+  float lc1 = q == 0 ? grow[idx2(gp)] : 0.f;
+  float sm_[4], lm_[4], P[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int g = 0; g < 4; ++g) lm_[g] = grow[idx3(gp, 4 * q + g)];
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  const int gl_ = (gp - 64 * cip) & 63;  // grand-parent within the CTA (the producer warp reads a valid one)
+  const float* lg = lstage + gl_ * 256;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) sm_[g] = sstage[gl_ * 16 + 4 * q + g];
+  float a2v[4][16];  // Lambda[gp, y, 4q + i]: this thread's A2 rows (held across the barrier below)
+  float amax1 = 0.f, amax2 = 0.f;
+#pragma unroll
+  for (int y = 0; y < 16; ++y) {
+    const float sy = sstage[gl_ * 16 + y];
+    const float4 l4 = *reinterpret_cast<const float4*>(lg + y * 16 + 4 * q);
+    a2v[0][y] = l4.x; a2v[1][y] = l4.y; a2v[2][y] = l4.z; a2v[3][y] = l4.w;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      P[i] = fmaf(a2v[i][y], sy, P[i]);
+      amax2 = fmaxf(amax2, fabsf(a2v[i][y]));
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < 4; ++g)
+#pragma unroll
+    for (int z = 0; z < 16; ++z) amax1 = fmaxf(amax1, fabsf(lg[(4 * q + g) * 16 + z]));
+  const float s1 = tcu::pow2_scale(amax1), s2 = tcu::pow2_scale(amax2);
+  const float inv_s1 = 1.f / s1, inv_s2 = 1.f / s2;  // exact: powers of two
+  if (!producer) {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {  // A1 row (tile mt0 + g) = parent gp.(4q+g), K = leaf letter z
+#pragma unroll
+      for (int kg = 0; kg < 2; ++kg) {
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = lg[(4 * q + g) * 16 + 8 * kg + i];
+        const int off = (mt0 + g) * kRowHalves + tcu::kmajor_off16<2>(r, 8 * kg);
+        tcu::split8_store(v, s1, A1h + off, A1l + off);
+      }
+    }
+  }
+  __syncthreads();  // the staged leaf adjoints are read: their region becomes A2
+  if (!producer) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // A2 row (tile mt0 + i) = pair (gp, 4q+i), K = parent letter y
+#pragma unroll
+      for (int kg = 0; kg < 2; ++kg) {
+        float v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = a2v[i][8 * kg + k];
+        const int off = (mt0 + i) * kRowHalves + tcu::kmajor_off16<2>(r, 8 * kg);
+        tcu::split8_store(v, s2, A2h + off, A2l + off);
+      }
+    }
+  }
+  tcu::fence_async_smem();  // the A operands (generic-proxy stores) -> the tensor core's async proxy
+  tcu::fence_before();
+  __syncthreads();
+  tcu::fence_after();
+  const uint32_t tmem = *slot;
+  // chain letters' home lanes: ma / mb select v[la & 3] at q == la / 4 (resp. lb)
+  float ma[4], mb[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    ma[i] = (q == (la >> 2) && i == (la & 3)) ? 1.f : 0.f;
+    mb[i] = (q == (lb >> 2) && i == (lb & 3)) ? 1.f : 0.f;
+  }
+  const int my_letter = 4 * q + ((lane & 16) ? 2 : 0) + ((lane & 8) ? 1 : 0);
+
+  // ---- chunk pipeline (chunk k = the k-th processed, c = nchunks-1-k; buffers by k & 1).
+  // The producer warp stages samples two chunks ahead (cp.async), forms increments, B and
+  // 1/sigma one chunk ahead (mbarrier "ready" per buffer), issues each MMA group of chunk k+1
+  // as soon as the compute warps release that TMEM half in chunk k (named barriers 1, 2), and
+  // runs the chunk epilogue; the compute warps never wait on a CTA-wide barrier.
+  const int nchunks = (int)((M + CH - 1) / CH);
+  auto chunk_len = [&](int c) { return (int)(M - (int64_t)c * CH < CH ? M - (int64_t)c * CH : CH); };
+  auto stage = [&](int c, int db) {  // producer: cp.async of chunk c's samples into Xs[db]
+    const int rows = chunk_len(c) + 1;
+    const float* src = X + (b * L + (int64_t)c * CH) * D;
+    float* dst = Xsb(db);
+    for (int i = lane; i < rows * D; i += 32)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tcu::su32(dst + i)), "l"(src + i) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto prepare = [&](int c, int db, bool newest_in_flight) {  // producer: Dl[db], B[db], 1/sigma[db] of chunk c
+    if (newest_in_flight) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    const int cs = chunk_len(c);
+    const float* xs = Xsb(db);
+    float* dl = Dlb(db);
+    for (int i = lane; i < cs * D; i += 32) dl[i] = xs[i + D] - xs[i];
+    __syncwarp();
+    float v[16];  // lane = step row of B; rows past the chunk are zero
+#pragma unroll
+    for (int z = 0; z < 16; ++z) v[z] = lane < cs ? dl[lane * D + z] : 0.f;
+    float amax = 0.f;
+#pragma unroll
+    for (int z = 0; z < 16; ++z) amax = fmaxf(amax, fabsf(v[z]));
+    const float sc = tcu::pow2_scale(amax);
+    isig(db)[lane] = 1.f / sc;
+#pragma unroll
+    for (int kg = 0; kg < 2; ++kg) {
+      float w[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] = v[8 * kg + i];
+      const int off = tcu::kmajor_off16<2>(lane, 8 * kg);
+      tcu::split8_store(w, sc, Bhi(db) + off, Blo(db) + off);
+    }
+    tcu::fence_async_smem();  // generic-proxy writes of B -> the tensor core
+    __syncwarp();
+  };
+  auto issue = [&](int h, int db) {  // producer: the 48 MMAs of group h (steps 16h .. 16h+15) from B[db]
+    constexpr uint32_t id = tcu::idesc_f16(128, NG);
+    const uint64_t bh = tcu::smem_desc(tcu::su32(Bhi(db) + h * NG * 16), 128, 256);
+    const uint64_t bl = tcu::smem_desc(tcu::su32(Blo(db) + h * NG * 16), 128, 256);
+#pragma unroll
+    for (int mt = 0; mt < kTiles; ++mt) {
+      const uint32_t d1 = tmem + h * 256 + mt * NG, d2 = d1 + 128;
+      const uint64_t a1h = tcu::smem_desc(tcu::su32(A1h + mt * kRowHalves), 128, 256);
+      const uint64_t a1l = tcu::smem_desc(tcu::su32(A1l + mt * kRowHalves), 128, 256);
+      const uint64_t a2h = tcu::smem_desc(tcu::su32(A2h + mt * kRowHalves), 128, 256);
+      const uint64_t a2l = tcu::smem_desc(tcu::su32(A2l + mt * kRowHalves), 128, 256);
+      tcu::mma_ss_f16(d1, a1h, bh, id, 0u);
+      tcu::mma_ss_f16(d1, a1l, bh, id, 1u);
+      tcu::mma_ss_f16(d1, a1h, bl, id, 1u);
+      tcu::mma_ss_f16(d2, a2h, bh, id, 0u);
+      tcu::mma_ss_f16(d2, a2l, bh, id, 1u);
+      tcu::mma_ss_f16(d2, a2h, bl, id, 1u);
+    }
+    tcu::mma_commit(&mbar[h]);
+  };
+
+  // one reverse step s of the current chunk; rr = the TMEM products of step s (D1 then D2)
+  auto step = [&](int s, const float* dl, float is, const uint32_t (&rr)[8], float(*redw)[D]) {
+    const float* row = dl + s * D;
+    const float4 y4 = *reinterpret_cast<const float4*>(row + 4 * q);
+    const float dy[4] = {y4.x, y4.y, y4.z, y4.w};
+    const float d0 = row[la], d1 = row[lb];
+    // (a) reconstruct S_j = S_{j+1} (x) exp(-dX_j) on the chain and the parents
+    const float r0_3 = sc0 - d0 * (1.f / 3.f);
+    const float tr3 = fmaf(-0.5f * d1, r0_3, sc1);  // Tr(gp, 3): the exp(-dX) partial
+    const float nsc1 = fmaf(-d1, sc0 - 0.5f * d0, sc1);
+    sc0 = sc0 - d0;
+    sc1 = nsc1;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) sm_[g] = fmaf(-dy[g], tr3, sm_[g]);
+    // (b) forward partials from S_j: T(la, m), T(gp, m)
+    const float t0_2 = fmaf(0.5f, d0, sc0), t0_3 = fmaf(1.f / 3.f, d0, sc0), t0_4 = fmaf(0.25f, d0, sc0);
+    const float t1_3 = fmaf(0.5f * d1, t0_3, sc1);         // T(gp, 3)
+    const float t1_4 = fmaf(d1 * (1.f / 3.f), t0_4, sc1);  // T(gp, 4)
+    // the MMA products carry the operand scales: D1 = Tbar(u, 4) / k1, D2 = Q / k2
+    const float k1 = inv_s1 * is, k2 = inv_s2 * is;
+    const float pq = -tr3 * k2, gq = 0.5f * t1_4 * k2, gt = 0.5f * t1_4 * k1;
+    float v[4];
+    float tbp1 = 0.f, tbp2u = 0.f;  // Tbar(gp, 3), Tbar(gp, 4) / k1 from the parents
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      // leaf pairs: P_j = P_{j+1} - Tr(gp,3) Q_j;  gl = P_j + T(gp,4)/2 Q_j
+      const float Di = __uint_as_float(rr[4 + i]);
+      P[i] = fmaf(pq, Di, P[i]);
+      const float gl = fmaf(gq, Di, P[i]);
+      // parent u = gp.(4q+i): adjoint pull-back from its leaves, gradient of its letter
+      const float Du = __uint_as_float(rr[i]);  // Tbar(u, 4) / k1
+      const float lm = lm_[i];                  // Tbar(u, 3)
+      tbp1 = fmaf(dy[i], lm, tbp1);
+      tbp2u = fmaf(dy[i], Du, tbp2u);
+      const float gm = fmaf(lm, t1_3, gt * Du);
+      lm_[i] = fmaf(Du, k1, lm);
+      v[i] = gl + gm;
+    }
+    const float tbp2 = 0.5f * k1 * tbp2u;
+    // chain, deepest first (trunc_backward_kernel (c) with NC = 2): node gp (level 2), then la
+    float gc1, gc0;
+    {
+      const float n2 = lc1, n3 = tbp1, n4 = tbp2;  // Tbar(gp, m), m = 2..4
+      lc1 = n2 + n3 + n4;
+      gc1 = fmaf(n2, t0_2, fmaf(0.5f * n3, t0_3, (1.f / 3.f) * n4 * t0_4));
+      const float c2 = d1 * n2, c3 = 0.5f * d1 * n3, c4 = (1.f / 3.f) * d1 * n4;  // -> Tbar(la, m)
+      const float m1 = lc0;
+      lc0 = m1 + c2 + c3 + c4;
+      gc0 = fmaf(0.5f, c2, fmaf(1.f / 3.f, c3, fmaf(0.25f, c4, m1)));
+    }
+    // the quad's partial chain terms -> full per grand-parent, added at the lane of their letter
+    gc0 += __shfl_xor_sync(0xffffffffu, gc0, 1);
+    gc1 += __shfl_xor_sync(0xffffffffu, gc1, 1);
+    gc0 += __shfl_xor_sync(0xffffffffu, gc0, 2);
+    gc1 += __shfl_xor_sync(0xffffffffu, gc1, 2);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = fmaf(ma[i], gc0, fmaf(mb[i], gc1, v[i]));
+    // sum over the warp's 8 grand-parents (lane bits 4, 3, 2): transposing, one letter per lane pair
+    const bool u4 = (lane & 16) != 0, u3 = (lane & 8) != 0;
+    {
+      const float s0 = u4 ? v[0] : v[2], s1v = u4 ? v[1] : v[3];
+      const float k0 = u4 ? v[2] : v[0], k1v = u4 ? v[3] : v[1];
+      v[0] = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
+      v[1] = k1v + __shfl_xor_sync(0xffffffffu, s1v, 16);
+    }
+    {
+      const float snd = u3 ? v[0] : v[1], kp = u3 ? v[1] : v[0];
+      v[0] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
+    }
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 4);
+    if ((lane & 4) == 0) redw[s][my_letter] = v[0];
+  };
+
+  if (producer) {
+    if (nchunks > 0) {
+      stage(nchunks - 1, 0);
+      if (nchunks > 1) stage(nchunks - 2, 1);
+      prepare(nchunks - 1, 0, nchunks > 1);
+      if (nchunks > 2) stage(nchunks - 3, 0);
+      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(tcu::su32(&mbar[2])) : "memory");
+      issue(1, 0);
+      issue(0, 0);
+    }
+    for (int k = 0; k < nchunks; ++k) {
+      const int c = nchunks - 1 - k, db = k & 1;
+      if (k + 1 < nchunks) {  // increments / B of chunk k+1 (its samples were staged two chunks ago)
+        prepare(c - 1, db ^ 1, k + 2 < nchunks);
+        if (k + 3 < nchunks) stage(c - 3, db ^ 1);
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(tcu::su32(&mbar[2 + (db ^ 1)]))
+                     : "memory");
+      }
+      tcu::bar_sync(1, kBlock);  // chunk k's group 1 is read: its TMEM half takes chunk k+1's group 1
+      tcu::fence_after();
+      if (k + 1 < nchunks) issue(1, db ^ 1);
+      tcu::bar_sync(2, kBlock);  // chunk k's group 0 is read and red[db] is complete
+      tcu::fence_after();
+      if (k + 1 < nchunks) issue(0, db ^ 1);
+      // chunk epilogue: fixed-order sum over the 8 compute warps -> partial[path part][j][z]
+      const int cs = chunk_len(c);
+      for (int i = lane; i < cs * D; i += 32) {
+        const int s = i / D, z = i % D;
+        const float a0 = red[db][0][s][z] + red[db][1][s][z], a1 = red[db][2][s][z] + red[db][3][s][z];
+        const float a2 = red[db][4][s][z] + red[db][5][s][z], a3 = red[db][6][s][z] + red[db][7][s][z];
+        partial[(((b - b0) * CPP + cip) * M + (int64_t)c * CH + s) * D + z] = (a0 + a1) + (a2 + a3);
+      }
+    }
+  } else {
+    for (int k = 0; k < nchunks; ++k) {
+      const int c = nchunks - 1 - k, db = k & 1;
+      const int cs = chunk_len(c);
+      tcu::mbar_wait(&mbar[2 + db], (uint32_t)((k >> 1) & 1));  // increments of chunk k ready
+      const float* dl = Dlb(db);
+      const float* is = isig(db);
+      float(*redw)[D] = red[db][warp];
+#pragma unroll 1
+      for (int h = 1; h >= 0; --h) {
+        const int lo = NG * h, hi = (cs < NG * (h + 1) ? cs : NG * (h + 1)) - 1;
+        tcu::mbar_wait(&mbar[h], (uint32_t)(k & 1));  // group h's products are in TMEM
+        tcu::fence_after();
+        if (hi >= lo) {
+          const uint32_t base = tmem + lane_addr + h * 256 - lo;
+          auto load = [&](uint32_t (&rr)[8], int s) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) rr[g] = tcu::tmem_ld1(base + (mt0 + g) * NG + s);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) rr[4 + i] = tcu::tmem_ld1(base + 128 + (mt0 + i) * NG + s);
+          };
+          // two register sets: step s computes from one while step s-1's TMEM loads land in the other
+          uint32_t ra[8], rb[8];
+          load(ra, hi);
+          ld_wait8(ra);
+          int s = hi;
+#pragma unroll 1
+          for (; s - 1 >= lo; s -= 2) {
+            load(rb, s - 1);
+            step(s, dl, is[s], ra, redw);
+            ld_wait8(rb);
+            if (s - 2 >= lo) load(ra, s - 2);
+            step(s - 1, dl, is[s - 1], rb, redw);
+            if (s - 2 >= lo) ld_wait8(ra);
+          }
+          if (s == lo) step(s, dl, is[s], ra, redw);
+        }
+        tcu::fence_before();
+        tcu::bar_arrive(h == 1 ? 1 : 2, kBlock);
+      }
+    }
+  }
+  tcu::fence_before();
+  __syncthreads();
+  if (producer) tcu::tmem_dealloc<512>(tmem);
+}
+
+}  // namespace pq
+}  // namespace trunc
+}  // namespace sigb
