@@ -490,6 +490,15 @@ def run_ours(args) -> None:
              "hbm_frac": bytes_path * B * args.steps / sec / 1e9 / float(peaks.get("hbm_gbs", 6456.8)),
              "launch_ms": k_ms / k_n, "launches": k_n, "peak_source": peak_src, "peak_ubench": peak_ub,
              "traffic_source": src, "ncu_exec": ncu_exec(kname, args.config)}
+        if kname == "trunc_pq_backward_kernel":
+            # both leaf sums on the tensor pipe: D1 = Lambda.dX (over z) and D2 = Lambda^T.dX (over y), each
+            # parents x d letters per path-step, 3 fp16 passes (hi.hi + lo.hi + hi.lo), 2 flop per MAC
+            leaf_parents = int((np.asarray(ws.lengths) == cfg["depth"] - 1).sum())
+            tc_flop = 2 * 3 * 2 * leaf_parents * d * M * B * args.steps / sec / 1e12
+            f16_peak = float(peaks.get("bf16_tflops", 2250.0))
+            r["tensor"] = {"achieved": tc_flop, "peak": f16_peak, "unit": "TFLOP/s", "frac": tc_flop / f16_peak,
+                           "peak_source": "MEASURED_PEAKS.json bf16_tflops (kind::f16 runs at the bf16 rate)",
+                           "note": "scaled 3-pass fp16 leaf products on tcgen05 (csrc/sigb_trunc_pq.cuh)"}
         if kname == "trunc_tc_forward_kernel":
             # leaf level on the tensor pipe: 3xTF32 (3 MMAs) x parents x d letters x 2 flop per path-step
             leaf_parents = int((np.asarray(ws.lengths) == cfg["depth"] - 1).sum())
@@ -514,6 +523,8 @@ def run_ours(args) -> None:
         kb_name, kf_name = "sigjit_bwd", "sigjit_fwd"
     if tc_fwd:
         kf_name = "trunc_tc_forward_kernel"  # leaf level on the tensor cores (csrc/sigb_trunc_tc.cuh)
+        kb_name = {"2": "trunc_pq_backward_kernel", "1": "trunc_backward_kernel"}.get(
+            os.environ.get("SIGB_TRUNC_TC_BWD", "2"), "trunc_backward_kernel")  # csrc/sigb_trunc_pq.cuh
     roof_b = roof(kb_name, f_bwd_path, min_bwd_path, kb_ms, kb_n, bytes_bwd)
     roof_f = roof(kf_name, f_fwd_path, min_fwd_path, kf_ms, kf_n, bytes_fwd)
     dominant = roof_b if (roof_b and kb_ms >= kf_ms) else roof_f
