@@ -69,7 +69,10 @@ def parse_args(argv=None):
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    p.add_argument("--config", default="c5", choices=("c1", "c2", "c3", "c4", "c5"))
+    p.add_argument("--config", default="c5", choices=("c1", "c2", "c3", "c4", "c5", "p1", "p2"),
+                   help="BASELINE.json configs c1-c5; p1/p2 = pathsig's H200 training rows (PAPER.md:429-449)")
+    p.add_argument("--precision", default="config", choices=("config", "fp64"),
+                   help="fp64: run the config in float64 (the reference's backward contract, backward.py:166-167)")
     p.add_argument("--batch", type=int, default=0, help="override the per-rank batch (profiling only)")
     p.add_argument("--weak", action="store_true", help="every rank runs the config's whole batch (weak scaling)")
     p.add_argument("--strong", action="store_true", help="(default) shard one fixed global batch across the ranks")
@@ -250,10 +253,12 @@ def cpu_threads() -> int:
         return os.cpu_count() or 1
 
 
-def workload(name: str):
+def workload(name: str, precision: str = "config"):
     from tests.configs import CONFIGS
 
     cfg = dict(CONFIGS[name])
+    if precision == "fp64":
+        cfg["dtype"] = np.float64
     return cfg
 
 
@@ -309,7 +314,7 @@ def run_reference(args) -> None:
     import paper_2602_24066_b200 as sk
     from tests.configs import build_wordset
 
-    cfg = workload(args.config)
+    cfg = workload(args.config, args.precision)
     ws = build_wordset(args.config, sk)
     threads = cpu_threads()
     for _ in range(args.warmup):
@@ -373,7 +378,7 @@ def run_ours(args) -> None:
         return float(t.item())
 
     _lib.set_kernel_policy(args.policy)
-    cfg = workload(args.config)
+    cfg = workload(args.config, args.precision)
     ws = build_wordset(args.config, sk)
     plan = ws.plan(dev)
     from paper_2602_24066_b200.sharding import shard_range
@@ -552,7 +557,7 @@ def run_ours(args) -> None:
         del src, dst
 
     # -- end to end: public API, host buffers --------------------------------------------
-    e2e = e2e_fwd = None
+    e2e = e2e_fwd = e2e_dropin = None
     if not args.no_e2e:
         del S, g, dXo
         torch.cuda.empty_cache()
@@ -647,6 +652,24 @@ def run_ours(args) -> None:
         e2e_fwd = {"value": Bn * world / (fms / 1e3), "unit": "paths/s", "ms_per_step": fms,
                    "paths_per_rank": Bn, "h2d_bytes_per_step": int(Xn.nbytes), "d2h_bytes_per_step": Bn * W * s_el,
                    "api": "signature_forward(numpy) -> CoefficientBatch(numpy); host-synchronous wall clock"}
+        # the reference's drop-in pair on host arrays: signature_forward + signature_backward, the backward
+        # in float64 as its contract requires (backward.py:166-167); host upstream of the same shape
+        Bd = min(Bn, max(1, (1 << 30) // (W * 8)))
+        Xd = Xn[:Bd]
+        gd = np.random.default_rng(7).standard_normal((Bd, W))
+        sk.signature_backward(Xd[:1], ws, gd[:1])
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            sk.signature_forward(Xd, ws)
+            sk.signature_backward(Xd, ws, gd)
+        dms = max_over_ranks((time.perf_counter() - t0) * 1e3 / reps)
+        e2e_dropin = {"value": Bd * world / (dms / 1e3), "unit": "paths/s", "ms_per_step": dms, "paths_per_rank": Bd,
+                      "h2d_bytes_per_step": int(Xd.nbytes + 8 * Bd * W + 8 * Xd.size),
+                      "d2h_bytes_per_step": int(Bd * W * s_el + 8 * Bd * (L - 1) * d + 8 * Xd.size),
+                      "api": "signature_forward(numpy) + signature_backward(numpy, float64 upstream) -> GradBatch; "
+                             "the backward always computes in float64 (the reference contract)"}
 
     # -- CPU baseline (rank 0, N = 1 only) -------------------------------------------------
     cpu = None
@@ -674,9 +697,13 @@ def run_ours(args) -> None:
                            plan.kernel_kind, "level-synchronous trie")},
             "fwd": {"value": fwd_value, "unit": "paths/s", "ms_per_step": fwd_ms / args.steps},
             "roofline": dominant, "roofline_fwd": roof_f if dominant is not roof_f else roof_b,
-            "cpu_baseline": cpu, "e2e": e2e, "e2e_fwd": e2e_fwd, "gather": gather,
+            "cpu_baseline": cpu, "e2e": e2e, "e2e_fwd": e2e_fwd, "e2e_dropin_fwd_bwd": e2e_dropin, "gather": gather,
             "gpu_launches": launches, "clocks": clk,
         }
+        if "paper_ms" in cfg:  # pathsig's own H200 training time for this row (context, not a baseline)
+            line["paper_context"] = {"row": cfg["paper_row"], "pathsig_h200_ms": cfg["paper_ms"],
+                                     "pathsig_h200_paths_per_s": cfg["B"] / (cfg["paper_ms"] / 1e3),
+                                     "source": "/root/reference/PAPER.md:429-449 (training time, fwd+bwd)"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

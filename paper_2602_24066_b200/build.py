@@ -97,7 +97,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 def precompile_shipped() -> None:
     """NVRTC-compile the generated kernels of the shipped small word set (config 3,
-    fp32 forward + backward) into jit_cache/ next to the library, host-only, so a
+    fp32 and fp64, forward + backward) into jit_cache/ next to the library, host-only, so a
     device process (smoke, tests, bench) loads cubins instead of compiling."""
     import json
 
@@ -116,8 +116,10 @@ def precompile_shipped() -> None:
                 os.remove(os.path.join(cache, name))
     with open(words) as f:
         ws = build_custom([tuple(w) for w in json.load(f)["words"]], 16)
-    for backward in (False, True):
-        _lib.jit_precompile(np.asarray(ws.codes), np.asarray(ws.lengths), ws.d, _lib.SIGB_F32, backward)
+    # fp32 for the autograd path, fp64 for the drop-in numpy API (signature_backward is float64)
+    for dtype in (_lib.SIGB_F32, _lib.SIGB_F64):
+        for backward in (False, True):
+            _lib.jit_precompile(np.asarray(ws.codes), np.asarray(ws.lengths), ws.d, dtype, backward)
 
 
 def build_ubench(force: bool = False) -> str:

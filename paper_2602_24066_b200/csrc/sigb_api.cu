@@ -294,8 +294,8 @@ extern "C" int sigb_backward_workspace_size(const sigb_plan* plan, int dtype, in
   DeviceGuard guard(plan->device);
   if (ckpt_stride < 0) return fail(SIGB_ERR_DOMAIN, "checkpoint stride must be >= 1");
   if (B == 0 || L == 1) { *bytes = 0; return SIGB_OK; }
-  if (use_trunc(plan) && ckpt_stride == 0) {
-    *bytes = trunc::backward_workspace(dtype, plan->d, plan->trunc_depth, B, L);
+  if (use_trunc(plan)) {  // checkpoint_stride included (replay + reload in the truncated kernels)
+    *bytes = trunc::backward_workspace(dtype, plan->d, plan->trunc_depth, B, L, ckpt_stride);
     return SIGB_OK;
   }
   if (use_jit(plan) && ckpt_stride == 0 &&
@@ -331,10 +331,10 @@ extern "C" int sigb_backward(const sigb_plan* plan, int dtype, const void* d_X, 
   if (ckpt_stride < 0) return fail(SIGB_ERR_DOMAIN, "checkpoint stride must be >= 1");
   if (!s_is_state && !plan->prefix_closed)
     return fail(SIGB_ERR_DOMAIN, "word set is not prefix-closed: pass the closure state from sigb_forward");
-  if (use_trunc(plan) && ckpt_stride == 0 && B > 0 && L > 1) {
+  if (use_trunc(plan) && B > 0 && L > 1) {
     if (s_is_state) { s_ld = plan->Wc; s_col0 = 0; }
     return trunc::backward(dtype, plan->d, plan->trunc_depth, d_X, B, L, d_S, s_ld, s_col0, d_g, g_ld, g_col0, d_work,
-                           work_bytes, d_dX, d_dinc, (cudaStream_t)stream);
+                           work_bytes, d_dX, d_dinc, (cudaStream_t)stream, ckpt_stride);
   }
   if (use_jit(plan) && ckpt_stride == 0 && B > 0 && L > 1) {
     if (s_is_state) { s_ld = plan->Wc; s_col0 = 0; }

@@ -224,10 +224,12 @@ namespace trunc {
 bool supported(int64_t d, int depth);
 int forward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L, const int64_t* bounds, int64_t K,
             void* out, int64_t out_ld, int64_t out_col0, int include_empty, cudaStream_t stream);
-size_t backward_workspace(int dtype, int64_t d, int depth, int64_t B, int64_t L);
+// stride > 0: the reference's checkpoint_stride (backward.py:183-199): a forward replay stores the
+// prefix levels every `stride` steps and the reverse sweep reloads them there
+size_t backward_workspace(int dtype, int64_t d, int depth, int64_t B, int64_t L, int64_t stride = 0);
 int backward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L, const void* S, int64_t s_ld,
              int64_t s_col0, const void* g, int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, void* dX,
-             void* dinc, cudaStream_t stream);
+             void* dinc, cudaStream_t stream, int64_t stride = 0);
 }  // namespace trunc
 int launch_wordset_tables(const uint64_t* d_codes, const int64_t* d_lengths, int64_t W, int64_t d,
                           int64_t max_len, int64_t* d_letters, int64_t* d_prefix, int64_t* d_suffix,

@@ -799,6 +799,19 @@ struct Pending {
   std::string cubin, err;
 };
 
+namespace {
+// Background compiles still running when the process exits would race NVRTC's own teardown
+// (a crash at exit): the library's static destructor -- run before libnvrtc's, which it depends
+// on -- waits for them (bounded).
+std::atomic<int> g_inflight{0};
+struct InflightGuard {
+  ~InflightGuard() {
+    for (int i = 0; i < 24000 && g_inflight.load(std::memory_order_acquire) > 0; ++i)
+      std::this_thread::sleep_for(std::chrono::milliseconds(5));
+  }
+} g_inflight_guard;
+}  // namespace
+
 bool wait_default() {
   static const bool sync_env = getenv("SIGB_JIT_SYNC") && atoi(getenv("SIGB_JIT_SYNC")) != 0;
   return g_policy == 4 || sync_env;
@@ -839,6 +852,7 @@ int ensure(sigb_plan* p, int dtype, bool backward, bool wait) {
     pd = std::make_shared<Pending>();
     std::shared_ptr<Pending> job = pd;
     // host-only work (no CUDA calls): the thread owns its share of the job and may outlive the plan
+    g_inflight.fetch_add(1, std::memory_order_acq_rel);
     std::thread([job, src]() {
       std::string out;
       const int rc = compile(src, out);
@@ -849,6 +863,7 @@ int ensure(sigb_plan* p, int dtype, bool backward, bool wait) {
         job->err = "NVRTC compile of the word-set kernel failed";
         job->state.store(2, std::memory_order_release);
       }
+      g_inflight.fetch_sub(1, std::memory_order_acq_rel);
     }).detach();
   }
   if (wait)

@@ -46,19 +46,26 @@ int fwd(const T* X, int64_t B, int64_t L, const int64_t* bounds, int64_t K, T* o
   return SIGB_OK;
 }
 
+// checkpoint words per path for checkpoint_stride > 0: levels 1..N-1 at M / stride + 1 steps
+template <int D, int N, int G>
+size_t ckpt_words(int64_t L, int64_t stride) {
+  return stride > 0 ? (size_t)((L - 1) / stride + 1) * (size_t)Cfg<D, N, G>::off(N) : 0;
+}
+
 template <typename T, int D, int N, int G>
-int64_t bwd_chunk(int64_t B, int64_t L) {
+int64_t bwd_chunk(int64_t B, int64_t L, int64_t stride = 0) {
   using C = Cfg<D, N, G>;
-  const size_t per_path = sizeof(T) * (size_t)C::CPP * (L - 1) * D;
+  const size_t per_path = sizeof(T) * ((size_t)C::CPP * (L - 1) * D + ckpt_words<D, N, G>(L, stride));
   int64_t chunk = per_path ? (int64_t)(kPartialBudget / per_path) : B;
   chunk = std::max<int64_t>(C::PPC, chunk - chunk % C::PPC);
   return std::min<int64_t>(chunk, ((B + C::PPC - 1) / C::PPC) * C::PPC);
 }
 
 template <typename T, int D, int N, int G>
-size_t bwd_workspace(int64_t B, int64_t L) {
+size_t bwd_workspace(int64_t B, int64_t L, int64_t stride = 0) {
   using C = Cfg<D, N, G>;
-  return sizeof(T) * (size_t)bwd_chunk<T, D, N, G>(B, L) * C::CPP * (L - 1) * D;
+  return sizeof(T) * (size_t)bwd_chunk<T, D, N, G>(B, L, stride) *
+         ((size_t)C::CPP * (L - 1) * D + ckpt_words<D, N, G>(L, stride));
 }
 
 template <typename T>
@@ -86,25 +93,27 @@ __global__ void trunc_sample_grads(const T* __restrict__ partial, int64_t Bc, in
 
 template <typename T, int D, int N, int G>
 int bwd(const T* X, int64_t B, int64_t L, const T* S, int64_t s_ld, int64_t s_col0, const T* g, int64_t g_ld,
-        int64_t g_col0, void* work, size_t work_bytes, T* dX, T* dinc, cudaStream_t stream) {
+        int64_t g_col0, void* work, size_t work_bytes, T* dX, T* dinc, cudaStream_t stream, int64_t stride) {
   using C = Cfg<D, N, G>;
   using RG = RedGeom<D, N, G>;
   const int64_t M = L - 1;
-  const int64_t chunk = bwd_chunk<T, D, N, G>(B, L);
-  if (work_bytes < bwd_workspace<T, D, N, G>(B, L) || !work)
+  const int64_t chunk = bwd_chunk<T, D, N, G>(B, L, stride);
+  if (work_bytes < bwd_workspace<T, D, N, G>(B, L, stride) || !work)
     return fail(SIGB_ERR_DOMAIN, "backward workspace too small");
   size_t smem = RG::template smem_bytes<T>();
   // experiment knob: SIGB_TRUNC_ASYNC=0/1 forces the staging mode (default: D >= 16)
   static const int force_async = getenv("SIGB_TRUNC_ASYNC") ? atoi(getenv("SIGB_TRUNC_ASYNC")) : -1;
   const bool async = force_async < 0 ? (D >= 16) : force_async != 0;
-  auto kern = async ? trunc_backward_kernel<T, D, N, G, true> : trunc_backward_kernel<T, D, N, G, false>;
+  auto kern = stride > 0 ? (async ? trunc_backward_kernel<T, D, N, G, true, false, true>
+                                  : trunc_backward_kernel<T, D, N, G, false, false, true>)
+                         : (async ? trunc_backward_kernel<T, D, N, G, true> : trunc_backward_kernel<T, D, N, G, false>);
   bool pq_kernel = false;
   if constexpr (std::is_same<T, float>::value && D == 16 && N == 4 && G == 4) {
     // leaf level on the tensor cores.  SIGB_TRUNC_TC_BWD selects: 2 (default) the P/Q kernel
     // (sigb_trunc_pq.cuh, both leaf sums on tcgen05), 1 the parent pull-back only on tcgen05
     // (TcBwd), 0 the CUDA-core kernel (A/B experiments, parity tests)
     const char* e = getenv("SIGB_TRUNC_TC_BWD");
-    const int mode = e ? atoi(e) : 2;
+    const int mode = stride > 0 ? 0 : (e ? atoi(e) : 2);  // checkpoint reloads: the CUDA-core kernel
     if (mode == 2 && force_async != 0) {
       pq_kernel = true;
       smem = pq::kSmem;
@@ -117,9 +126,15 @@ int bwd(const T* X, int64_t B, int64_t L, const T* S, int64_t s_ld, int64_t s_co
   }
   if (!pq_kernel) SIGB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   T* partial = (T*)work;
+  T* ckpt = stride > 0 ? partial + (size_t)chunk * C::CPP * M * D : nullptr;
   for (int64_t b0 = 0; b0 < B; b0 += chunk) {
     const int64_t Bc = std::min(chunk, B - b0);
     const int64_t grid = C::CPP > 1 ? Bc * C::CPP : (Bc + C::PPC - 1) / C::PPC;
+    if (stride > 0) {
+      count_launch();
+      trunc_ckpt_kernel<T, D, N, G><<<(unsigned)grid, C::THREADS, 0, stream>>>(X, B, L, b0, stride, ckpt);
+      SIGB_CUDA_TRY(cudaGetLastError());
+    }
     count_launch(2);
     timing_begin(1, stream);
     if constexpr (std::is_same<T, float>::value && D == 16 && N == 4 && G == 4) {
@@ -127,9 +142,11 @@ int bwd(const T* X, int64_t B, int64_t L, const T* S, int64_t s_ld, int64_t s_co
         pq::trunc_pq_backward_kernel<<<(unsigned)grid, pq::kBlock, smem, stream>>>(X, B, L, b0, S, s_ld, s_col0, g,
                                                                                      g_ld, g_col0, partial);
       else
-        kern<<<(unsigned)grid, C::THREADS, smem, stream>>>(X, B, L, b0, S, s_ld, s_col0, g, g_ld, g_col0, partial);
+        kern<<<(unsigned)grid, C::THREADS, smem, stream>>>(X, B, L, b0, S, s_ld, s_col0, g, g_ld, g_col0, partial,
+                                                           ckpt, stride);
     } else {
-      kern<<<(unsigned)grid, C::THREADS, smem, stream>>>(X, B, L, b0, S, s_ld, s_col0, g, g_ld, g_col0, partial);
+      kern<<<(unsigned)grid, C::THREADS, smem, stream>>>(X, B, L, b0, S, s_ld, s_col0, g, g_ld, g_col0, partial,
+                                                         ckpt, stride);
     }
     timing_end(1, stream);
     SIGB_CUDA_TRY(cudaGetLastError());
@@ -179,10 +196,11 @@ int forward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L
   return fail(SIGB_ERR_UNSUPPORTED, "no truncated kernel for this (d, depth)");
 }
 
-size_t backward_workspace(int dtype, int64_t d, int depth, int64_t B, int64_t L) {
-#define X(D_, N_, GF_, GB_)                                                                       \
-  if (d == D_ && depth == N_)                                                                     \
-    return dtype == SIGB_F32 ? bwd_workspace<float, D_, N_, GB_>(B, L) : bwd_workspace<double, D_, N_, GB_>(B, L);
+size_t backward_workspace(int dtype, int64_t d, int depth, int64_t B, int64_t L, int64_t stride) {
+#define X(D_, N_, GF_, GB_)                                                                                \
+  if (d == D_ && depth == N_)                                                                              \
+    return dtype == SIGB_F32 ? bwd_workspace<float, D_, N_, GB_>(B, L, stride)                             \
+                             : bwd_workspace<double, D_, N_, GB_>(B, L, stride);
   SIGB_TRUNC_CASES(X)
 #undef X
   return 0;
@@ -190,14 +208,14 @@ size_t backward_workspace(int dtype, int64_t d, int depth, int64_t B, int64_t L)
 
 int backward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L, const void* S, int64_t s_ld,
              int64_t s_col0, const void* g, int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, void* dX,
-             void* dinc, cudaStream_t stream) {
+             void* dinc, cudaStream_t stream, int64_t stride) {
 #define X(D_, N_, GF_, GB_)                                                                                       \
   if (d == D_ && depth == N_) {                                                                                   \
     if (dtype == SIGB_F32)                                                                                        \
       return bwd<float, D_, N_, GB_>((const float*)X, B, L, (const float*)S, s_ld, s_col0, (const float*)g, g_ld,  \
-                                    g_col0, work, work_bytes, (float*)dX, (float*)dinc, stream);                  \
+                                    g_col0, work, work_bytes, (float*)dX, (float*)dinc, stream, stride);          \
     return bwd<double, D_, N_, GB_>((const double*)X, B, L, (const double*)S, s_ld, s_col0, (const double*)g,     \
-                                   g_ld, g_col0, work, work_bytes, (double*)dX, (double*)dinc, stream);           \
+                                   g_ld, g_col0, work, work_bytes, (double*)dX, (double*)dinc, stream, stride);   \
   }
   SIGB_TRUNC_CASES(X)
 #undef X

@@ -373,6 +373,63 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
   if (include_empty && f.t == 0) orow[-1] = T(1);
 }
 
+// Checkpoint replay for checkpoint_stride > 0 (reference backward.py:183-199, _kernels.py:122-141):
+// the forward sweep without the leaf level, storing S_{0,t_k} of every non-leaf word (levels
+// 1..N-1, canonical indices [0, off(N))) at k = 0, stride, 2 stride, ... into
+// ckpt[(b - b0)][k / stride][word].  The reverse sweep reloads these instead of its
+// exp(-dX) reconstruction at those steps.
+template <typename T, int D, int N, int G>
+__global__ void __launch_bounds__(Cfg<D, N, G>::THREADS)
+    trunc_ckpt_kernel(const T* __restrict__ X, int64_t B, int64_t L, int64_t b0, int64_t stride,
+                      T* __restrict__ ckpt) {
+  using C = Cfg<D, N, G>;
+  constexpr int CH = kChunkFwd;
+  constexpr int64_t NW = C::off(N);  // non-leaf words per checkpoint
+  __shared__ __align__(16) T Xs[C::PPC * (CH + 1) * D];
+  __shared__ __align__(16) T Dl[C::PPC * CH * D];
+  const int64_t cta = blockIdx.x + (C::CPP > 1 ? b0 * C::CPP : b0 / C::PPC);
+  const Frag<D, N, G> f(cta, threadIdx.x);
+  const int64_t b_first = C::CPP > 1 ? f.b : cta * C::PPC;
+  const int64_t M = L - 1, nck = M / stride + 1;
+  const bool live = f.b < B;
+  State<T, D, N, G> st;
+#pragma unroll
+  for (int k = 0; k < C::NC; ++k) st.ch[k] = T(0);
+#pragma unroll
+  for (int g = 0; g < G; ++g) st.mid[g] = T(0);
+  T* cb = ckpt + (live ? f.b - b0 : 0) * nck * NW;
+  auto store = [&](int64_t k) {
+    if (!live) return;
+    T* row = cb + k * NW;
+#pragma unroll
+    for (int c = 0; c < C::NC; ++c)
+      if (f.chain_owner(c)) row[f.chain_index(c)] = st.ch[c];
+#pragma unroll
+    for (int g = 0; g < G; ++g) row[f.mid_index(g)] = st.mid[g];
+  };
+  store(0);
+  Prefetch<T, D, C::PPC, CH, C::THREADS> pf;  // the next chunk's samples load under this chunk's steps
+  if (M > 0) pf.load(X, b_first, B, L, nullptr, 1, 0, (int)(M < CH ? M : CH));
+  for (int64_t j0 = 0; j0 < M; j0 += CH) {
+    const int cs = (int)(M - j0 < CH ? M - j0 : CH);
+    pf.commit(Xs, cs);
+    __syncthreads();
+    for (int i = threadIdx.x; i < C::PPC * cs * D; i += blockDim.x) {
+      const int pc = i / (cs * D), r = i % (cs * D);
+      Dl[pc * CH * D + r] = Xs[pc * (CH + 1) * D + r + D] - Xs[pc * (CH + 1) * D + r];
+    }
+    __syncthreads();
+    if (j0 + CH < M) pf.load(X, b_first, B, L, nullptr, 1, j0 + CH, (int)(M - j0 - CH < CH ? M - j0 - CH : CH));
+    const T* rows = Dl + f.pc * CH * D;
+    for (int s = 0; s < cs; ++s) {
+      StepIncr<T, D, N, G> in;
+      in.load(rows + s * D, f, T(1));
+      chen_step<T, D, N, G, false>(st, in);
+      if ((j0 + s + 1) % stride == 0) store((j0 + s + 1) / stride);
+    }
+  }
+}
+
 // Transposing butterfly: V values over the WIDTH lanes of each aligned group.
 // On return v[0] holds the group sum of value index `idx` (returned); lanes
 // that differ only in the plain-sum bits hold the same index.
@@ -491,11 +548,11 @@ struct TcBwd {
 
 // Backward.  grid: one CTA per (CTA-part of a path) -- paths [b0, b0 + nb).
 // partial layout: [(b - b0) * CPP + cip][M][D].
-template <typename T, int D, int N, int G, bool ASYNC = (D >= 16), bool TC = false>
-__global__ void __launch_bounds__(Cfg<D, N, G>::THREADS, TC ? 2 : 1)
+template <typename T, int D, int N, int G, bool ASYNC = (D >= 16), bool TC = false, bool CK = false>
+__global__ void __launch_bounds__(Cfg<D, N, G>::THREADS, (TC || (sizeof(T) == 4 && D == 16)) ? 2 : 1)
     trunc_backward_kernel(const T* __restrict__ X, int64_t B, int64_t L, int64_t b0, const T* __restrict__ Sin,
                           int64_t s_ld, int64_t s_col0, const T* __restrict__ gup, int64_t g_ld, int64_t g_col0,
-                          T* __restrict__ partial) {
+                          T* __restrict__ partial, const T* __restrict__ ckpt = nullptr, int64_t stride = 0) {
   using C = Cfg<D, N, G>;
   using RG = RedGeom<D, N, G>;
   constexpr int NC = C::NC;
@@ -615,6 +672,22 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS, TC ? 2 : 1)
     tmem = *tmem_slot;
   }
   const int nchunks = (int)((M + RG::CH - 1) / RG::CH);
+  T ck_ch[NCc], ck_mid[G];  // checkpoint_stride (CK): the next reload, prefetched
+  int ck_rem = 0;
+  int64_t ck_k = 0;
+  const T* ck_base = nullptr;
+  if (CK) {
+    ck_rem = (int)((M - 1) % stride);  // the sweep's first step j = M - 1
+    ck_k = (M - 1) / stride;
+    ck_base = ckpt + (live ? f.b - b0 : 0) * ((L - 1) / stride + 1) * Cfg<D, N, G>::off(N);
+    if (live) {
+      const T* row = ck_base + ck_k * Cfg<D, N, G>::off(N);
+#pragma unroll
+      for (int k = 0; k < NC; ++k) ck_ch[k] = row[f.chain_index(k)];
+#pragma unroll
+      for (int g = 0; g < G; ++g) ck_mid[g] = row[f.mid_index(g)];
+    }
+  }
   // ASYNC: double-buffered cp.async staging of chunk c-1 while chunk c computes
   if (ASYNC && nchunks > 0)
     issue_samples<T, D, C::PPC, RG::CH>(X, b_first, B, L, (nchunks - 1) * RG::CH,
@@ -705,6 +778,28 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS, TC ? 2 : 1)
         }
       }
       if (!(TC && SIGB_ABLATE == 6)) chen_step<T, D, N, G, false>(st, in);
+      if (CK) {
+        // checkpoint_stride: S_{0,t_j} from the forward replay instead of the reconstruction,
+        // loaded one step ahead (ck_*) so the reload does not stall the sweep.  ck_rem = j mod
+        // stride and ck_k = j / stride are carried down the sweep (no 64-bit division per step).
+        if (ck_rem == 0) {
+#pragma unroll
+          for (int k = 0; k < NC; ++k) st.ch[k] = ck_ch[k];
+#pragma unroll
+          for (int g = 0; g < G; ++g) st.mid[g] = ck_mid[g];
+        }
+        const int nrem = ck_rem == 0 ? (int)stride - 1 : ck_rem - 1;
+        const int64_t nk = ck_rem == 0 ? ck_k - 1 : ck_k;
+        if (nrem == 0 && nk >= 0 && live) {
+          const T* row = ck_base + nk * Cfg<D, N, G>::off(N);
+#pragma unroll
+          for (int k = 0; k < NC; ++k) ck_ch[k] = row[f.chain_index(k)];
+#pragma unroll
+          for (int g = 0; g < G; ++g) ck_mid[g] = row[f.mid_index(g)];
+        }
+        ck_rem = nrem;
+        ck_k = nk;
+      }
       // (b) forward partials from S_{0,t_j}
       if constexpr (!TC) {
 #pragma unroll

@@ -22,6 +22,15 @@ CONFIGS = {
                B=4096, L=1024, dtype=np.float32, bwd=True),
     "c5": dict(seed=5, kind="truncated", d=16, depth=4, B=65536, L=512, dtype=np.float32, bwd=True),
 }
+# pathsig's own training benchmark rows (H200): context
+# workloads for bench.py, not BASELINE configs.  (B, M, d) with M increments = L - 1.
+PAPER_CONFIGS = {
+    "p1": dict(seed=11, kind="truncated", d=4, depth=6, B=64, L=1001, dtype=np.float32, bwd=True,
+               paper_ms=6.45, paper_row="(64, 1000, 4) N=6: pathsig 6.45 ms on H200"),
+    "p2": dict(seed=12, kind="truncated", d=10, depth=4, B=256, L=201, dtype=np.float32, bwd=True,
+               paper_ms=9.83, paper_row="(256, 200, 10) N=4: pathsig 9.83 ms on H200"),
+}
+CONFIGS.update(PAPER_CONFIGS)
 
 
 def brownian(seed: int, B: int, L: int, d: int, chunk: int | None = None) -> np.ndarray:

@@ -153,3 +153,30 @@ def test_fp32_autograd_bench_inputs_c3_c4(name):
     S = St.detach().cpu().numpy()
     dX = Xt.grad.cpu().numpy()
     _check_paths(name, X32, S, dX, g, _shard_picks(B, worlds=(2, 4)), TOL32, "fp32_autograd_bench_inputs")
+
+
+@pytest.mark.parametrize("stride", [1, 5, 7])
+def test_checkpoint_stride_truncated_kernels(stride):
+    """checkpoint_stride (reference backward.py:183-199, _kernels.py:122-141) on the truncated kernels:
+    a replay stores the prefix levels every `stride` steps, the reverse sweep reloads them there.
+    fp64 drop-in at the c5 word set against the oracle's own stride-`stride` backward (1e-10) and
+    against stride 0 (the reference's test_backward.py:225-234 bar, 1e-9); fp32 autograd too."""
+    cfg = CONFIGS["c5"]
+    ws = build_wordset("c5", sk)
+    B, L = 3, 77
+    X = brownian(cfg["seed"], B, L, cfg["d"])
+    g = np.random.default_rng(105).standard_normal((B, len(ws)))
+    ck = sk.signature_backward(X, ws, g, checkpoint_stride=stride).path_grads
+    plain = sk.signature_backward(X, ws, g).path_grads
+    _, dref = ora.backward(X, ws.codes, ws.lengths, cfg["d"], g, stride=stride)
+    assert ora.rel_err(ck, dref) <= TOL64
+    assert ora.rel_err(ck, plain) <= 1e-9
+    Xt = torch.from_numpy(X.astype(np.float32)).cuda().requires_grad_(True)
+    sk.signature(Xt, ws, checkpoint_stride=stride).backward(torch.from_numpy(g).float().cuda())
+    assert ora.rel_err(Xt.grad.cpu().numpy(), dref) <= TOL32
+    for name in ("c1", "c2"):  # other truncated instantiations
+        w2 = build_wordset(name, sk)
+        X2 = brownian(CONFIGS[name]["seed"], 2, 40, w2.d)
+        g2 = np.random.default_rng(7).standard_normal((2, len(w2)))
+        _, d2 = ora.backward(X2, w2.codes, w2.lengths, w2.d, g2, stride=stride)
+        assert ora.rel_err(sk.signature_backward(X2, w2, g2, checkpoint_stride=stride).path_grads, d2) <= TOL64
