@@ -485,7 +485,8 @@ def run_ours(args) -> None:
             return None
         sec = k_ms / 1e3
         achieved = flop_path * B * args.steps / sec / 1e12  # per rank, per launch average
-        tr, src = ncu_traffic(kname, args.config)
+        ckey = args.config + ("_fp64" if args.precision == "fp64" else "")  # ncu captures are per dtype
+        tr, src = ncu_traffic(kname, ckey)
         per_launch_paths = B * args.steps / k_n
         r = {"bound": "fma", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
              "frac": achieved / peak, "frac_alg": achieved / peak,
@@ -494,7 +495,7 @@ def run_ours(args) -> None:
              "algorithmic_bytes": bytes_path * per_launch_paths, "flop_per_launch": flop_path * per_launch_paths,
              "hbm_frac": bytes_path * B * args.steps / sec / 1e9 / float(peaks.get("hbm_gbs", 6456.8)),
              "launch_ms": k_ms / k_n, "launches": k_n, "peak_source": peak_src, "peak_ubench": peak_ub,
-             "traffic_source": src, "ncu_exec": ncu_exec(kname, args.config)}
+             "traffic_source": src, "ncu_exec": ncu_exec(kname, ckey)}
         if kname == "trunc_pq_backward_kernel":
             # both leaf sums on the tensor pipe: D1 = Lambda.dX (over z) and D2 = Lambda^T.dX (over y), each
             # parents x d letters per path-step, 3 fp16 passes (hi.hi + lo.hi + hi.lo), 2 flop per MAC
