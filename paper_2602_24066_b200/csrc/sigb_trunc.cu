@@ -27,10 +27,12 @@ int fwd(const T* X, int64_t B, int64_t L, const int64_t* bounds, int64_t K, T* o
     // SIGB_TRUNC_TC=0 selects the register kernel (A/B experiments, parity tests).
     const char* e = getenv("SIGB_TRUNC_TC");
     if (!(e && atoi(e) == 0) && !bounds) {
+      SIGB_CUDA_TRY(cudaFuncSetAttribute(tc::trunc_tc_forward_kernel<D, N>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kFwdSmem));
       count_launch();
       timing_begin(0, stream);
-      tc::trunc_tc_forward_kernel<D, N><<<(unsigned)grid, tc::kThreadsTc, 0, stream>>>(X, B, L, out, out_ld, out_col0,
-                                                                                       include_empty);
+      tc::trunc_tc_forward_kernel<D, N><<<(unsigned)grid, tc::kThreadsTc, tc::kFwdSmem, stream>>>(
+          X, B, L, out, out_ld, out_col0, include_empty);
       timing_end(0, stream);
       SIGB_CUDA_TRY(cudaGetLastError());
       return SIGB_OK;

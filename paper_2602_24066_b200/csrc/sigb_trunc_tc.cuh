@@ -56,6 +56,21 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, u
 
 __device__ __forceinline__ int kmajor_off(int row, int k) { return tcu::kmajor_off32<2>(row, k); }  // rows x 8 steps
 
+// shared memory of the forward (dynamic): samples, increments and B operands are double-buffered
+// by chunk; the output staging tile (the CTA's 1,024 x 16 leaves, then its parents) reuses nothing
+constexpr int kRounds = kChunkTc / kStepsPerMma;   // MMA rounds per chunk (4)
+constexpr int fXs = 0;                              // [2][(CH + 1) * 16] samples
+constexpr int fDl = fXs + 2 * 4 * (kChunkTc + 1) * 16;   // [2][CH * 16] increments
+constexpr int fB = fDl + 2 * 4 * kChunkTc * 16;    // [2][kRounds][hi | lo][16 x 8] tf32 (128-byte aligned)
+constexpr int fBar = fB + 2 * kRounds * 2 * 4 * 16 * kStepsPerMma;  // mbarriers: MMA done, ready[2]
+constexpr int fSlot = fBar + 32;
+constexpr int fOut = (fSlot + 16 + 1023) & ~1023;  // [1,024 parents][16] leaves, staged for coalesced stores
+constexpr size_t kFwdSmem = fOut + 4 * 1024 * 16;
+
+// Forward.  Warps 0-7 (compute): the register fragment without its leaves, A = the parents'
+// partials per 8-step round via tcgen05.st.  Warp 8 (producer): stages the samples two chunks
+// ahead (cp.async), forms each chunk's increments and the four rounds' B operands (dX hi / lo)
+// one chunk ahead, and issues each round's 24 MMAs once the compute warps have stored A.
 template <int D, int N>
 __global__ void __launch_bounds__(kThreadsTc, 2)
     trunc_tc_forward_kernel(const float* __restrict__ X, int64_t B, int64_t L, float* __restrict__ out,
@@ -65,36 +80,75 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
   static_assert(D == 16 && C::PPC == 1 && C::THREADS == kComputeThreads, "one path per CTA, 16 letters");
   constexpr int NC = C::NC;
   constexpr int CH = kChunkTc;
-  __shared__ __align__(16) float Xs[(CH + 1) * D];
-  __shared__ __align__(16) float Dl[CH * D];
-  __shared__ __align__(128) float Bs[2 * D * kStepsPerMma];  // rows 0-15 dX_hi, 16-31 dX_lo; K = 8 steps
-  __shared__ __align__(8) uint64_t mbar;
-  __shared__ uint32_t tmem_base;
+  extern __shared__ __align__(1024) unsigned char smf[];
+  auto Xsb = [&](int db) { return reinterpret_cast<float*>(smf + fXs) + db * (CH + 1) * D; };
+  auto Dlb = [&](int db) { return reinterpret_cast<float*>(smf + fDl) + db * CH * D; };
+  auto Bsb = [&](int db, int r, int lo) {
+    return reinterpret_cast<float*>(smf + fB) + ((db * kRounds + r) * 2 + lo) * 16 * kStepsPerMma;
+  };
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smf + fBar);  // [0] MMA round done, [1 + db] chunk ready
+  uint32_t* slot = reinterpret_cast<uint32_t*>(smf + fSlot);
+  float* stage_out = reinterpret_cast<float*>(smf + fOut);
 
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool producer = warp == kComputeThreads / 32;
   const int64_t M = L - 1;
-  const int nch = (int)((M + kStepsPerMma - 1) / kStepsPerMma);
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)),
-                 "n"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  const int nch = (int)((M + kStepsPerMma - 1) / kStepsPerMma);  // MMA rounds
+  const int nchunks = (int)((M + CH - 1) / CH);
+  const int64_t bpath = blockIdx.x / C::CPP;
+  if (producer) {
+    tcu::tmem_alloc<kTmemCols>(slot);
+    if (lane == 0) {
+      tcu::mbar_init(&mbar[0], 1);
+      tcu::mbar_init(&mbar[1], 32);
+      tcu::mbar_init(&mbar[2], 32);
+    }
   }
-  if (tid == 32) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mbar)));
-    asm volatile("fence.mbarrier_init.release.cluster;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
+  tcu::fence_before();
   __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = tmem_base;
+  tcu::fence_after();
+  const uint32_t tmem = *slot;
 
-  if (warp == kComputeThreads / 32) {
-    // ---- MMA warp ----
+  if (producer) {
+    auto chunk_len = [&](int c) { return (int)(M - (int64_t)c * CH < CH ? M - (int64_t)c * CH : CH); };
+    auto stage = [&](int c) {  // cp.async of chunk c's samples into Xs[c & 1]
+      const int rows = chunk_len(c) + 1;
+      const float* src = X + (bpath * L + (int64_t)c * CH) * D;
+      float* dst = Xsb(c & 1);
+      for (int i = lane; i < rows * D; i += 32)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(su32(dst + i)), "l"(src + i) : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto prepare = [&](int c, bool newest_in_flight) {  // Dl and the 4 rounds' B of chunk c, then "ready"
+      if (newest_in_flight) asm volatile("cp.async.wait_group 1;" ::: "memory");
+      else asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
+      const int cs = chunk_len(c), db = c & 1;
+      const float* xs = Xsb(db);
+      float* dl = Dlb(db);
+      for (int i = lane; i < CH * D; i += 32) dl[i] = i < cs * D ? xs[i + D] - xs[i] : 0.f;
+      __syncwarp();
+      for (int i = lane; i < CH * D; i += 32) {  // B[r]: rows = letters (hi 0-15, lo in its own tile), K = 8 steps
+        const int sidx = i / D, n = i % D, r = sidx / kStepsPerMma, k = sidx % kStepsPerMma;
+        const float x = dl[i], h = tf32_hi(x);
+        Bsb(db, r, 0)[kmajor_off(n, k)] = h;
+        Bsb(db, r, 1)[kmajor_off(n, k)] = x - h;
+      }
+      tcu::fence_async_smem();
+      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(su32(&mbar[1 + db])) : "memory");
+    };
+    if (nchunks > 0) {
+      stage(0);
+      if (nchunks > 1) stage(1);
+      prepare(0, nchunks > 1);
+      if (nchunks > 2) stage(2);
+    }
     constexpr uint32_t id16 = idesc_tf32(128, 16);
-    const uint64_t b_hi = smem_desc(su32(Bs), 128, 256);
-    const uint64_t b_lo = smem_desc(su32(Bs + 16 * kStepsPerMma), 128, 256);
     for (int c = 0; c < nch; ++c) {
-      bar_sync(1, kThreadsTc);  // A and B of chunk c written
+      const int ck = c / kRounds, r = c % kRounds, db = ck & 1;
+      const uint64_t b_hi = smem_desc(su32(Bsb(db, r, 0)), 128, 256);
+      const uint64_t b_lo = smem_desc(su32(Bsb(db, r, 1)), 128, 256);
+      bar_sync(1, kThreadsTc);  // A of round c stored
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt) {
@@ -103,7 +157,11 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
         mma_ts(d, a + 8, b_hi, id16, 1u);           // A_lo dX_hi
         mma_ts(d, a, b_lo, id16, 1u);               // A_hi dX_lo
       }
-      mma_commit(&mbar);
+      mma_commit(&mbar[0]);
+      if (r == 0 && ck + 1 < nchunks) {  // the next chunk, under this chunk's rounds
+        prepare(ck + 1, ck + 2 < nchunks);
+        if (ck + 3 < nchunks) stage(ck + 3);
+      }
     }
   } else {
     // ---- compute warps: the register kernel's fragment without its leaves ----
@@ -115,18 +173,13 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
     for (int g = 0; g < G; ++g) mid[g] = 0.f;
     const uint32_t lane_addr = (uint32_t)(32 * (warp & 3)) << 16;
     const int mt0 = (warp >> 2) * G;  // this thread's parents g sit in tiles mt0 + g
-    Prefetch<float, D, 1, CH, kComputeThreads> pf;
-    if (M > 0) pf.load(X, f.b, B, L, nullptr, 1, 0, (int)(M < CH ? M : CH));
     int c = 0;
-    for (int64_t j0 = 0; j0 < M; j0 += CH) {
-      const int cs = (int)(M - j0 < CH ? M - j0 : CH);
+    for (int ck = 0; ck < nchunks; ++ck) {
+      const int db = ck & 1;
+      const int cs = (int)(M - (int64_t)ck * CH < CH ? M - (int64_t)ck * CH : CH);
       const int cs8 = (cs + kStepsPerMma - 1) / kStepsPerMma * kStepsPerMma;
-      pf.commit(Xs, cs);
-      bar_sync(2, kComputeThreads);
-      for (int i = tid; i < cs8 * D; i += kComputeThreads) Dl[i] = i < cs * D ? Xs[i + D] - Xs[i] : 0.f;
-      bar_sync(2, kComputeThreads);
-      const int64_t j1 = j0 + CH;
-      if (j1 < M) pf.load(X, f.b, B, L, nullptr, 1, j1, (int)(M - j1 < CH ? M - j1 : CH));
+      mbar_wait(&mbar[1 + db], (uint32_t)((ck >> 1) & 1));  // increments of chunk ck ready
+      const float* Dl = Dlb(db);
       for (int s0 = 0; s0 < cs8; s0 += kStepsPerMma, ++c) {
         float ah[G][kStepsPerMma], al[G][kStepsPerMma];
 #pragma unroll
@@ -155,14 +208,8 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
             al[g][s] = tm - h;
           }
         }
-        if (c > 0) mbar_wait(&mbar, (uint32_t)((c - 1) & 1));  // chunk c-1's MMAs have read A and B
+        if (c > 0) mbar_wait(&mbar[0], (uint32_t)((c - 1) & 1));  // round c-1's MMAs have read A
         asm volatile("tcgen05.fence::after_thread_sync;");
-        if (tid < 128) {
-          const int n = tid & 15, k = tid >> 4;
-          const float x = Dl[(s0 + k) * D + n], h = tf32_hi(x);
-          Bs[kmajor_off(n, k)] = h;
-          Bs[kmajor_off(16 + n, k)] = x - h;
-        }
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           const uint32_t a = tmem + lane_addr + kACol + 16 * (mt0 + g);
@@ -174,50 +221,55 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
                        "f"(al[g][6]), "f"(al[g][7]));
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;");
         bar_arrive(1, kThreadsTc);
       }
     }
-    float leaf[G][D];
+    // epilogue: leaves from TMEM, staged in shared memory [parent within the CTA][letter], then
+    // written with consecutive threads on consecutive words (the CTA's leaves are one contiguous
+    // block of 16,384 words; its parents one block of 1,024)
+    const int pl0 = (f.gp - (int)(f.cip * (kComputeThreads / C::Q))) * D + f.q * G;  // first parent in the CTA
     if (nch > 0) {
-      mbar_wait(&mbar, (uint32_t)((nch - 1) & 1));
+      mbar_wait(&mbar[0], (uint32_t)((nch - 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        uint32_t r[D];
+        uint32_t rg[D];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "=r"(rg[0]), "=r"(rg[1]), "=r"(rg[2]), "=r"(rg[3]), "=r"(rg[4]), "=r"(rg[5]), "=r"(rg[6]), "=r"(rg[7]),
+              "=r"(rg[8]), "=r"(rg[9]), "=r"(rg[10]), "=r"(rg[11]), "=r"(rg[12]), "=r"(rg[13]), "=r"(rg[14]),
+              "=r"(rg[15])
             : "r"(tmem + lane_addr + 16 * (mt0 + g)));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        float4* dst = reinterpret_cast<float4*>(stage_out + (pl0 + g) * D);
 #pragma unroll
-        for (int z = 0; z < D; ++z) leaf[g][z] = __uint_as_float(r[z]);
+        for (int z = 0; z < D; z += 4)
+          dst[z / 4] = make_float4(__uint_as_float(rg[z]), __uint_as_float(rg[z + 1]), __uint_as_float(rg[z + 2]),
+                                   __uint_as_float(rg[z + 3]));
       }
     } else {
 #pragma unroll
       for (int g = 0; g < G; ++g)
 #pragma unroll
-        for (int z = 0; z < D; ++z) leaf[g][z] = 0.f;
+        for (int z = 0; z < D; ++z) stage_out[(pl0 + g) * D + z] = 0.f;
     }
+    bar_sync(2, kComputeThreads);  // the CTA's leaf block is staged
     if (f.b < B) {
       float* orow = out + f.b * out_ld + out_col0;
+      float* leaves = orow + C::off(N) + (int64_t)f.cip * (kComputeThreads / C::Q) * D * D;
+      for (int i = tid; i < (kComputeThreads / C::Q) * D * D; i += kComputeThreads) leaves[i] = stage_out[i];
 #pragma unroll
       for (int k = 0; k < NC; ++k)
         if (f.chain_owner(k)) orow[f.chain_index(k)] = ch[k];
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        orow[f.mid_index(g)] = mid[g];
-#pragma unroll
-        for (int z = 0; z < D; ++z) orow[f.leaf_index(g, z)] = leaf[g][z];
-      }
+      for (int g = 0; g < G; ++g) orow[f.mid_index(g)] = mid[g];
       if (include_empty && f.t == 0) orow[-1] = 1.f;
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
+  if (producer) tcu::tmem_dealloc<kTmemCols>(tmem);
 }
 
 }  // namespace tc
