@@ -32,7 +32,7 @@ namespace tc {
 
 constexpr int kStepsPerMma = 8;  // tf32 K per tcgen05.mma
 constexpr int kComputeThreads = 256;
-constexpr int kThreadsTc = kComputeThreads + 32;  // + the MMA warp
+constexpr int kThreadsTc = kComputeThreads + 64;  // + the MMA warp + the staging warp
 constexpr int kTmemCols = 256;
 constexpr int kACol = 128;
 constexpr int kChunkTc = 32;  // steps of samples staged per round
@@ -91,7 +91,8 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
   float* stage_out = reinterpret_cast<float*>(smf + fOut);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const bool producer = warp == kComputeThreads / 32;
+  const bool producer = warp == kComputeThreads / 32;      // issues the MMAs
+  const bool stager = warp == kComputeThreads / 32 + 1;    // samples, increments, B operands
   const int64_t M = L - 1;
   const int nch = (int)((M + kStepsPerMma - 1) / kStepsPerMma);  // MMA rounds
   const int nchunks = (int)((M + CH - 1) / CH);
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
   tcu::fence_after();
   const uint32_t tmem = *slot;
 
-  if (producer) {
+  if (stager) {
     auto chunk_len = [&](int c) { return (int)(M - (int64_t)c * CH < CH ? M - (int64_t)c * CH : CH); };
     auto stage = [&](int c) {  // cp.async of chunk c's samples into Xs[c & 1]
       const int rows = chunk_len(c) + 1;
@@ -143,12 +144,20 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
       prepare(0, nchunks > 1);
       if (nchunks > 2) stage(2);
     }
+    for (int ck = 1; ck < nchunks; ++ck) {
+      // chunk ck's buffers are free once the compute warps have stored round 0 of chunk ck-1
+      // (they read chunk ck-2's increments no more) and its MMAs read B of chunk ck-2 no more
+      bar_sync(3, kComputeThreads + 32);
+      prepare(ck, ck + 1 < nchunks);
+      if (ck + 2 < nchunks) stage(ck + 2);
+    }
+  } else if (producer) {
     constexpr uint32_t id16 = idesc_tf32(128, 16);
     for (int c = 0; c < nch; ++c) {
       const int ck = c / kRounds, r = c % kRounds, db = ck & 1;
       const uint64_t b_hi = smem_desc(su32(Bsb(db, r, 0)), 128, 256);
       const uint64_t b_lo = smem_desc(su32(Bsb(db, r, 1)), 128, 256);
-      bar_sync(1, kThreadsTc);  // A of round c stored
+      bar_sync(1, kComputeThreads + 32);  // A of round c stored
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt) {
@@ -158,10 +167,6 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
         mma_ts(d, a, b_lo, id16, 1u);               // A_hi dX_lo
       }
       mma_commit(&mbar[0]);
-      if (r == 0 && ck + 1 < nchunks) {  // the next chunk, under this chunk's rounds
-        prepare(ck + 1, ck + 2 < nchunks);
-        if (ck + 3 < nchunks) stage(ck + 3);
-      }
     }
   } else {
     // ---- compute warps: the register kernel's fragment without its leaves ----
@@ -222,7 +227,9 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;");
-        bar_arrive(1, kThreadsTc);
+        bar_arrive(1, kComputeThreads + 32);
+        // round 0 of chunk ck stored: the stager may refill the buffers of chunk ck-1 with chunk ck+1
+        if (s0 == 0 && ck + 1 < nchunks) bar_arrive(3, kComputeThreads + 32);
       }
     }
     // epilogue: leaves from TMEM, staged in shared memory [parent within the CTA][letter], then
