@@ -296,7 +296,37 @@ __global__ void __launch_bounds__(kBlock, 1)
     in.is = isg[s];
     return in;
   };
-  auto step = [&](int s, const Inc& in, const uint32_t (&rr)[8], float(*redw)[D]) {
+  // a step's letter sums before the cross-lane reduction: the reduction of step s is issued after
+  // the arithmetic of step s-1 (source order), so its shuffle latency overlaps that arithmetic
+  struct Sums {
+    float v[4], gc0, gc1;
+  };
+  auto reduce = [&](Sums& u, int s, float(*redw)[D]) {
+    float gc0 = u.gc0, gc1 = u.gc1;
+    float* v = u.v;
+    // the quad's partial chain terms -> full per grand-parent, added at the lane of their letter
+    gc0 += __shfl_xor_sync(0xffffffffu, gc0, 1);
+    gc1 += __shfl_xor_sync(0xffffffffu, gc1, 1);
+    gc0 += __shfl_xor_sync(0xffffffffu, gc0, 2);
+    gc1 += __shfl_xor_sync(0xffffffffu, gc1, 2);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = fmaf(ma[i], gc0, fmaf(mb[i], gc1, v[i]));
+    // sum over the warp's 8 grand-parents (lane bits 4, 3, 2): transposing, one letter per lane pair
+    const bool u4 = (lane & 16) != 0, u3 = (lane & 8) != 0;
+    {
+      const float s0 = u4 ? v[0] : v[2], s1v = u4 ? v[1] : v[3];
+      const float k0 = u4 ? v[2] : v[0], k1v = u4 ? v[3] : v[1];
+      v[0] = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
+      v[1] = k1v + __shfl_xor_sync(0xffffffffu, s1v, 16);
+    }
+    {
+      const float snd = u3 ? v[0] : v[1], kp = u3 ? v[1] : v[0];
+      v[0] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
+    }
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 4);
+    if ((lane & 4) == 0) redw[s][my_letter] = v[0];
+  };
+  auto step = [&](const Inc& in, const uint32_t (&rr)[8]) -> Sums {
     const float dy[4] = {in.y.x, in.y.y, in.y.z, in.y.w};
     const float d0 = in.d0, d1 = in.d1, is = in.is;
     // (a) reconstruct S_j = S_{j+1} (x) exp(-dX_j) on the chain and the parents
@@ -314,7 +344,8 @@ __global__ void __launch_bounds__(kBlock, 1)
     // the MMA products carry the operand scales: D1 = Tbar(u, 4) / k1, D2 = Q / k2
     const float k1 = inv_s1 * is, k2 = inv_s2 * is;
     const float pq = -tr3 * k2, gq = 0.5f * t1_4 * k2, gt = 0.5f * t1_4 * k1;
-    float v[4];
+    Sums out;
+    float* v = out.v;
     float tbp1 = 0.f, tbp2u = 0.f;  // Tbar(gp, 3), Tbar(gp, 4) / k1 from the parents
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -343,27 +374,9 @@ __global__ void __launch_bounds__(kBlock, 1)
       lc0 = m1 + c2 + c3 + c4;
       gc0 = fmaf(0.5f, c2, fmaf(1.f / 3.f, c3, fmaf(0.25f, c4, m1)));
     }
-    // the quad's partial chain terms -> full per grand-parent, added at the lane of their letter
-    gc0 += __shfl_xor_sync(0xffffffffu, gc0, 1);
-    gc1 += __shfl_xor_sync(0xffffffffu, gc1, 1);
-    gc0 += __shfl_xor_sync(0xffffffffu, gc0, 2);
-    gc1 += __shfl_xor_sync(0xffffffffu, gc1, 2);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = fmaf(ma[i], gc0, fmaf(mb[i], gc1, v[i]));
-    // sum over the warp's 8 grand-parents (lane bits 4, 3, 2): transposing, one letter per lane pair
-    const bool u4 = (lane & 16) != 0, u3 = (lane & 8) != 0;
-    {
-      const float s0 = u4 ? v[0] : v[2], s1v = u4 ? v[1] : v[3];
-      const float k0 = u4 ? v[2] : v[0], k1v = u4 ? v[3] : v[1];
-      v[0] = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
-      v[1] = k1v + __shfl_xor_sync(0xffffffffu, s1v, 16);
-    }
-    {
-      const float snd = u3 ? v[0] : v[1], kp = u3 ? v[1] : v[0];
-      v[0] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
-    }
-    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 4);
-    if ((lane & 4) == 0) redw[s][my_letter] = v[0];
+    out.gc0 = gc0;
+    out.gc1 = gc1;
+    return out;
   };
 
   if (producer) {
@@ -425,21 +438,37 @@ __global__ void __launch_bounds__(kBlock, 1)
           load(ra, hi);
           Inc ia = fetch(hi, dl, is), ib;
           ld_wait8(ra);
-          int s = hi;
+          // two register sets: a step computes from one while the next step's TMEM loads land in the
+          // other; each step's arithmetic precedes the previous step's reduction in program order
+          if (hi - 1 >= lo) {
+            load(rb, hi - 1);
+            ib = fetch(hi - 1, dl, is);
+          }
+          Sums pend = step(ia, ra);
+          int s = hi - 1;
 #pragma unroll 1
           for (; s - 1 >= lo; s -= 2) {
-            load(rb, s - 1);
-            ib = fetch(s - 1, dl, is);
-            step(s, ia, ra, redw);
             ld_wait8(rb);
+            load(ra, s - 1);
+            ia = fetch(s - 1, dl, is);
+            Sums cur = step(ib, rb);
+            reduce(pend, s + 1, redw);
+            ld_wait8(ra);
             if (s - 2 >= lo) {
-              load(ra, s - 2);
-              ia = fetch(s - 2, dl, is);
+              load(rb, s - 2);
+              ib = fetch(s - 2, dl, is);
             }
-            step(s - 1, ib, rb, redw);
-            if (s - 2 >= lo) ld_wait8(ra);
+            pend = step(ia, ra);
+            reduce(cur, s, redw);
           }
-          if (s == lo) step(s, ia, ra, redw);
+          if (s == lo) {
+            ld_wait8(rb);
+            Sums cur = step(ib, rb);
+            reduce(pend, s + 1, redw);
+            pend = cur;
+            s -= 1;
+          }
+          reduce(pend, s + 1, redw);
         }
         tcu::fence_before();
         tcu::bar_arrive(h == 1 ? 1 : 2, kBlock);
