@@ -99,6 +99,10 @@ __device__ __forceinline__ uint32_t tmem_ld1(uint32_t addr) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(addr));
   return r;
 }
+// two consecutive 32-bit columns of the warp's lanes: column c -> lo, c + 1 -> hi
+__device__ __forceinline__ void tmem_ld2(uint32_t addr, uint32_t& lo, uint32_t& hi) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(addr));
+}
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // K-major no-swizzle offsets (in elements) of (row, k) for 4-byte and 2-byte elements

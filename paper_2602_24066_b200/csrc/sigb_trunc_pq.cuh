@@ -84,6 +84,11 @@ __device__ __forceinline__ void ld_wait8(uint32_t (&r)[8]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;"
                : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]));
 }
+__device__ __forceinline__ void ld_wait16(uint32_t (&a)[8], uint32_t (&b)[8]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
+                 "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]), "+r"(b[6]), "+r"(b[7]));
+}
 
 __global__ void __launch_bounds__(kBlock, 1)
     trunc_pq_backward_kernel(const float* __restrict__ X, int64_t B, int64_t L, int64_t b0,
@@ -147,15 +152,13 @@ __global__ void __launch_bounds__(kBlock, 1)
   float sc0 = srow[la], sc1 = srow[idx2(gp)];
   float lc0 = (q == 0 && lb == 0) ? grow[la] : 0.f;  // seeded once per chain node
   float lc1 = q == 0 ? grow[idx2(gp)] : 0.f;
-  float sm_[4], lm_[4], P[4] = {0.f, 0.f, 0.f, 0.f};
+  float lm_[4], P[4] = {0.f, 0.f, 0.f, 0.f};  // (the P/Q form never reads the parents' S_j)
 #pragma unroll
   for (int g = 0; g < 4; ++g) lm_[g] = grow[idx3(gp, 4 * q + g)];
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   const int gl_ = (gp - 64 * cip) & 63;  // grand-parent within the CTA (the producer warp reads a valid one)
   const float* lg = lstage + gl_ * 256;
-#pragma unroll
-  for (int g = 0; g < 4; ++g) sm_[g] = sstage[gl_ * 16 + 4 * q + g];
   float a2v[4][16];  // Lambda[gp, y, 4q + i]: this thread's A2 rows (held across the barrier below)
   float amax1 = 0.f, amax2 = 0.f;
 #pragma unroll
@@ -335,8 +338,6 @@ __global__ void __launch_bounds__(kBlock, 1)
     const float nsc1 = fmaf(-d1, sc0 - 0.5f * d0, sc1);
     sc0 = sc0 - d0;
     sc1 = nsc1;
-#pragma unroll
-    for (int g = 0; g < 4; ++g) sm_[g] = fmaf(-dy[g], tr3, sm_[g]);
     // (b) forward partials from S_j: T(la, m), T(gp, m)
     const float t0_2 = fmaf(0.5f, d0, sc0), t0_3 = fmaf(1.f / 3.f, d0, sc0), t0_4 = fmaf(0.25f, d0, sc0);
     const float t1_3 = fmaf(0.5f * d1, t0_3, sc1);         // T(gp, 3)
@@ -352,15 +353,14 @@ __global__ void __launch_bounds__(kBlock, 1)
       // leaf pairs: P_j = P_{j+1} - Tr(gp,3) Q_j;  gl = P_j + T(gp,4)/2 Q_j
       const float Di = __uint_as_float(rr[4 + i]);
       P[i] = fmaf(pq, Di, P[i]);
-      const float gl = fmaf(gq, Di, P[i]);
       // parent u = gp.(4q+i): adjoint pull-back from its leaves, gradient of its letter
       const float Du = __uint_as_float(rr[i]);  // Tbar(u, 4) / k1
       const float lm = lm_[i];                  // Tbar(u, 3)
       tbp1 = fmaf(dy[i], lm, tbp1);
       tbp2u = fmaf(dy[i], Du, tbp2u);
-      const float gm = fmaf(lm, t1_3, gt * Du);
+      // letter 4q+i: leaf term P_j + T(gp,4)/2 Q_j, parent term Tbar(u,3) T(gp,3) + Tbar(u,4) T(gp,4)/2
+      v[i] = fmaf(gt, Du, fmaf(lm, t1_3, fmaf(gq, Di, P[i])));
       lm_[i] = fmaf(Du, k1, lm);
-      v[i] = gl + gm;
     }
     const float tbp2 = 0.5f * k1 * tbp2u;
     // chain, deepest first (trunc_backward_kernel (c) with NC = 2): node gp (level 2), then la
@@ -427,43 +427,76 @@ __global__ void __launch_bounds__(kBlock, 1)
         tcu::fence_after();
         if (hi >= lo) {
           const uint32_t base = tmem + lane_addr + h * 256 - lo;
-          auto load = [&](uint32_t (&rr)[8], int s) {
+          // TMEM products of one step (x1) or of two consecutive steps in one load per tile (x2:
+          // column c -> rlo, c + 1 -> rhi)
+          auto load1 = [&](uint32_t (&rr)[8], int c) {
 #pragma unroll
-            for (int g = 0; g < 4; ++g) rr[g] = tcu::tmem_ld1(base + (mt0 + g) * NG + s);
+            for (int g = 0; g < 4; ++g) rr[g] = tcu::tmem_ld1(base + (mt0 + g) * NG + c);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) rr[4 + i] = tcu::tmem_ld1(base + 128 + (mt0 + i) * NG + s);
+            for (int i = 0; i < 4; ++i) rr[4 + i] = tcu::tmem_ld1(base + 128 + (mt0 + i) * NG + c);
           };
-          // two register sets: step s computes from one while step s-1's TMEM loads land in the other
-          uint32_t ra[8], rb[8];
-          load(ra, hi);
-          Inc ia = fetch(hi, dl, is), ib;
-          ld_wait8(ra);
-          // two register sets: a step computes from one while the next step's TMEM loads land in the
-          // other; each step's arithmetic precedes the previous step's reduction in program order
-          if (hi - 1 >= lo) {
-            load(rb, hi - 1);
-            ib = fetch(hi - 1, dl, is);
-          }
-          Sums pend = step(ia, ra);
+          auto load2 = [&](uint32_t (&rlo)[8], uint32_t (&rhi)[8], int c) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) tcu::tmem_ld2(base + (mt0 + g) * NG + c, rlo[g], rhi[g]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) tcu::tmem_ld2(base + 128 + (mt0 + i) * NG + c, rlo[4 + i], rhi[4 + i]);
+          };
+          // step hi alone; then pairs (s, s-1) whose products land in one register-set pair while the
+          // previous pair computes; each step's arithmetic precedes the previous step's reduction
+          uint32_t ra[8], rb[8], rc[8], rd[8];
+          Inc ia, ib, ic, id;
+          load1(ra, hi);
+          ia = fetch(hi, dl, is);
           int s = hi - 1;
-#pragma unroll 1
-          for (; s - 1 >= lo; s -= 2) {
-            ld_wait8(rb);
-            load(ra, s - 1);
-            ia = fetch(s - 1, dl, is);
-            Sums cur = step(ib, rb);
-            reduce(pend, s + 1, redw);
-            ld_wait8(ra);
-            if (s - 2 >= lo) {
-              load(rb, s - 2);
-              ib = fetch(s - 2, dl, is);
+          auto issue_next = [&](uint32_t (&rlo)[8], uint32_t (&rhi)[8], Inc& ilo, Inc& ihi, int top) {
+            if (top - 1 >= lo) {
+              load2(rlo, rhi, top - 1);
+              ihi = fetch(top, dl, is);
+              ilo = fetch(top - 1, dl, is);
+            } else if (top >= lo) {
+              load1(rhi, top);
+              ihi = fetch(top, dl, is);
             }
-            pend = step(ia, ra);
-            reduce(cur, s, redw);
+          };
+          issue_next(rc, rd, ic, id, s);
+          ld_wait8(ra);
+          Sums pend = step(ia, ra);
+          bool in_second = false;
+#pragma unroll 1
+          for (;;) {
+            if (s - 1 < lo) break;
+            ld_wait16(rc, rd);
+            issue_next(ra, rb, ia, ib, s - 2);
+            {
+              Sums cur = step(id, rd);
+              reduce(pend, s + 1, redw);
+              pend = step(ic, rc);
+              reduce(cur, s, redw);
+            }
+            s -= 2;
+            if (s - 1 < lo) {
+              in_second = true;
+              break;
+            }
+            ld_wait16(ra, rb);
+            issue_next(rc, rd, ic, id, s - 2);
+            {
+              Sums cur = step(ib, rb);
+              reduce(pend, s + 1, redw);
+              pend = step(ia, ra);
+              reduce(cur, s, redw);
+            }
+            s -= 2;
           }
-          if (s == lo) {
-            ld_wait8(rb);
-            Sums cur = step(ib, rb);
+          if (s == lo) {  // one step left, in rd (or rb)
+            Sums cur;
+            if (in_second) {
+              ld_wait8(rb);
+              cur = step(ib, rb);
+            } else {
+              ld_wait8(rd);
+              cur = step(id, rd);
+            }
             reduce(pend, s + 1, redw);
             pend = cur;
             s -= 1;
