@@ -58,6 +58,17 @@ int sigb_device_sm_count(void);
  * Process-wide; used by the tests to check both paths against the oracle.
  * (Policy 3, the round-1 level-slot kernels, was removed and is rejected.) */
 int sigb_set_kernel_policy(int policy);
+/* Tensor-core precision contract for float32 full truncations with d = 16, depth 4
+ * (config 5 shape).  on = 1 (default): the forward's leaf level runs as 3xTF32 on
+ * tcgen05 (hi/lo split of both operands, fp32 accumulation; measured <= 3.4e-6
+ * relative on S at c5) and the backward's two leaf sums as a scaled 3-pass fp16 split
+ * (power-of-two row / column scales, fp32 accumulation; <= 1.3e-6 relative on dL/dX),
+ * both well inside the 1e-4 float32 gate.  on = 0: the CUDA-core fp32 kernels
+ * (bitwise-reproducible against each other, ~15-60% slower).  float64 never uses
+ * the tensor cores.  Process-wide; the environment variables SIGB_TRUNC_TC=0 /
+ * SIGB_TRUNC_TC_BWD=0 select the CUDA-core kernels as well.  Returns the previous
+ * setting.  No reference counterpart (the reference is CPU-only, fp64 backward). */
+int sigb_set_tensor_cores(int on);
 /* Number of device kernels this library has launched (process-wide). */
 long long sigb_launch_count(void);
 /* CUDA-event timing of the main Chen kernels, recorded on the launch stream

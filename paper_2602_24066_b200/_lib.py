@@ -39,6 +39,7 @@ SIGNATURES = {
     "sigb_last_error": (ctypes.c_char_p, []),
     "sigb_device_sm_count": (ctypes.c_int, []),
     "sigb_set_kernel_policy": (_C, [_C]),
+    "sigb_set_tensor_cores": (_C, [_C]),
     "sigb_launch_count": (ctypes.c_longlong, []),
     "sigb_timing_enable": (_C, [_C]),
     "sigb_timing_read": (_C, [_C, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I)]),
@@ -96,6 +97,12 @@ def check(rc: int) -> None:
 def set_kernel_policy(policy: int) -> None:
     """0 auto (truncated > generated > fragment > level), 1 level only, 2 fragment first, 4 generated first."""
     check(lib().sigb_set_kernel_policy(int(policy)))
+
+
+def set_tensor_cores(on: bool) -> bool:
+    """Process-wide: tensor-core kernels for fp32 d=16 depth-4 truncations (default on); see
+    include/sigkit_b200.h sigb_set_tensor_cores for the precision contract.  Returns the previous value."""
+    return bool(lib().sigb_set_tensor_cores(1 if on else 0))
 
 
 def launch_count() -> int:

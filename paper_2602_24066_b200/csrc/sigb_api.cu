@@ -11,6 +11,7 @@ namespace sigb {
 
 static thread_local std::string g_last_error;
 int g_policy = 0;
+int g_tensor_cores = 1;
 static std::atomic<long long> g_launches{0};
 void count_launch(int n) { g_launches += n; }
 
@@ -199,6 +200,11 @@ extern "C" int sigb_set_kernel_policy(int policy) {
                                  "or 4 (generated kernels)");
   g_policy = policy;
   return SIGB_OK;
+}
+extern "C" int sigb_set_tensor_cores(int on) {
+  const int prev = g_tensor_cores;
+  g_tensor_cores = on ? 1 : 0;
+  return prev;
 }
 extern "C" long long sigb_launch_count(void) { return g_launches.load(); }
 

@@ -7,7 +7,6 @@ namespace sigb {
 namespace frag {
 namespace {
 
-constexpr size_t kPartialBudget = size_t(4) << 30;  // bytes of gradient partials per backward chunk
 
 FragDev dev_of(const sigb_plan* p) {
   FragDev f;
@@ -46,7 +45,7 @@ int fwd(const sigb_plan* p, const T* X, int64_t B, int64_t L, const int64_t* bou
 template <typename T>
 int64_t bwd_chunk(const sigb_plan* p, int64_t B, int64_t L) {
   const size_t per_path = sizeof(T) * (size_t)p->frag.cpp * (size_t)(L - 1) * p->d;
-  int64_t c = per_path ? (int64_t)(kPartialBudget / per_path) : B;
+  int64_t c = per_path ? (int64_t)(partial_budget() / 2 / per_path) : B;
   return std::max<int64_t>(1, std::min(c, B));
 }
 

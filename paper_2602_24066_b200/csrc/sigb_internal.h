@@ -203,8 +203,12 @@ struct DeviceGuard {
     if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
   }
 };
-// kernel-routing policy (sigb_set_kernel_policy) and launch counter
+// kernel-routing policy (sigb_set_kernel_policy), tensor-core switch (sigb_set_tensor_cores)
+// and launch counter
 extern int g_policy;
+extern int g_tensor_cores;
+// per-process byte budget for a backward's per-chunk workspace (partials, checkpoints)
+size_t partial_budget();
 void count_launch(int n = 1);
 // Optional CUDA-event timing of the main kernels (sigb_timing_enable):
 // `which` 0 = forward Chen kernel, 1 = backward Chen kernel (summed over batch chunks).

@@ -939,7 +939,6 @@ int forward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, 
 }
 
 namespace {
-constexpr size_t kPartialBudget = size_t(4) << 30;
 constexpr int kTT = 16;  // samples per sample-grads tile
 
 int groups_bwd(const sigb_plan* p, int dtype) {
@@ -951,7 +950,7 @@ int64_t pad32(int64_t n) { return (n + 31) / 32 * 32; }
 
 int64_t bwd_chunk(const sigb_plan* p, int dtype, int64_t B, int64_t L) {
   const size_t per_path = (dtype == SIGB_F32 ? 4 : 8) * (size_t)groups_bwd(p, dtype) * (size_t)(L - 1) * p->d;
-  int64_t c = per_path ? (int64_t)(kPartialBudget / per_path) : B;
+  int64_t c = per_path ? (int64_t)(partial_budget() / 2 / per_path) : B;
   c = std::min<int64_t>(std::max<int64_t>(32, c - c % 32), int64_t(1) << 20);
   return std::min<int64_t>(c, B);
 }

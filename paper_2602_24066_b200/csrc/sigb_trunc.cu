@@ -11,10 +11,26 @@
 #include "sigb_trunc_pq.cuh"
 
 namespace sigb {
+// Bytes of per-part gradient partials (+ checkpoints) per batch chunk of the backward: 1/16 of the
+// device's memory, at most 8 GiB (SIGB_PARTIAL_BUDGET_MB overrides).  Fixed per process, so the
+// workspace query and the launch always agree on the chunking.
+size_t partial_budget() {
+  static const size_t budget = [] {
+    if (const char* e = getenv("SIGB_PARTIAL_BUDGET_MB")) return std::max<size_t>(64, (size_t)atoll(e)) << 20;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || total_b == 0) {
+      cudaGetLastError();
+      return size_t(8) << 30;
+    }
+    return std::min<size_t>(size_t(8) << 30, std::max<size_t>(size_t(256) << 20, total_b / 16));
+  }();
+  return budget;
+}
+
 namespace trunc {
 namespace {
 
-constexpr size_t kPartialBudget = size_t(8) << 30;  // bytes of per-part gradient partials per chunk
+
 
 template <typename T, int D, int N, int G>
 int fwd(const T* X, int64_t B, int64_t L, const int64_t* bounds, int64_t K, T* out, int64_t out_ld, int64_t out_col0,
@@ -26,7 +42,7 @@ int fwd(const T* X, int64_t B, int64_t L, const int64_t* bounds, int64_t K, T* o
     // leaf level on the tensor cores (sigb_trunc_tc.cuh): c5 fwd 127.4 -> 92.5 ms.
     // SIGB_TRUNC_TC=0 selects the register kernel (A/B experiments, parity tests).
     const char* e = getenv("SIGB_TRUNC_TC");
-    if (!(e && atoi(e) == 0) && !bounds) {
+    if (g_tensor_cores && !(e && atoi(e) == 0) && !bounds) {
       SIGB_CUDA_TRY(cudaFuncSetAttribute(tc::trunc_tc_forward_kernel<D, N>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kFwdSmem));
       count_launch();
@@ -58,7 +74,7 @@ template <typename T, int D, int N, int G>
 int64_t bwd_chunk(int64_t B, int64_t L, int64_t stride = 0) {
   using C = Cfg<D, N, G>;
   const size_t per_path = sizeof(T) * ((size_t)C::CPP * (L - 1) * D + ckpt_words<D, N, G>(L, stride));
-  int64_t chunk = per_path ? (int64_t)(kPartialBudget / per_path) : B;
+  int64_t chunk = per_path ? (int64_t)(partial_budget() / per_path) : B;
   chunk = std::max<int64_t>(C::PPC, chunk - chunk % C::PPC);
   return std::min<int64_t>(chunk, ((B + C::PPC - 1) / C::PPC) * C::PPC);
 }
@@ -115,7 +131,7 @@ int bwd(const T* X, int64_t B, int64_t L, const T* S, int64_t s_ld, int64_t s_co
     // (sigb_trunc_pq.cuh, both leaf sums on tcgen05), 1 the parent pull-back only on tcgen05
     // (TcBwd), 0 the CUDA-core kernel (A/B experiments, parity tests)
     const char* e = getenv("SIGB_TRUNC_TC_BWD");
-    const int mode = stride > 0 ? 0 : (e ? atoi(e) : 2);  // checkpoint reloads: the CUDA-core kernel
+    const int mode = (stride > 0 || !g_tensor_cores) ? 0 : (e ? atoi(e) : 2);  // checkpoints: CUDA-core kernel
     if (mode == 2 && force_async != 0) {
       pq_kernel = true;
       smem = pq::kSmem;

@@ -110,3 +110,36 @@ def test_tc_backward_deterministic(monkeypatch):
     a = _autograd(X, ws, g, True, monkeypatch)
     b = _autograd(X, ws, g, True, monkeypatch)
     assert np.array_equal(a, b)
+
+
+def test_tensor_core_switch(monkeypatch):
+    """sigb_set_tensor_cores (include/sigkit_b200.h): off selects the CUDA-core fp32 kernels for the
+    c5-shaped set -- bitwise the SIGB_TRUNC_TC=0 / SIGB_TRUNC_TC_BWD=0 kernels -- on the tensor-core
+    ones; both inside the fp32 gate against the fp64 oracle."""
+    from paper_2602_24066_b200 import _lib
+
+    ws = sk.build_truncated(16, 4)
+    X = brownian(91, 4, 50, 16).astype(np.float32)
+    g = np.random.default_rng(92).standard_normal((4, len(ws))).astype(np.float32)
+    ref = ora.forward(X.astype(np.float64), ws.codes, ws.lengths, 16)
+    _, dref = ora.backward(X.astype(np.float64), ws.codes, ws.lengths, 16, g.astype(np.float64))
+
+    def run():
+        Xt = torch.from_numpy(X).cuda().requires_grad_(True)
+        S = sk.signature(Xt, ws)
+        S.backward(torch.from_numpy(g).cuda())
+        return S.detach().cpu().numpy(), Xt.grad.cpu().numpy()
+
+    prev = _lib.set_tensor_cores(False)
+    try:
+        S_cc, d_cc = run()
+    finally:
+        _lib.set_tensor_cores(prev)
+    S_tc, d_tc = run()
+    monkeypatch.setenv("SIGB_TRUNC_TC", "0")
+    monkeypatch.setenv("SIGB_TRUNC_TC_BWD", "0")
+    S_env, d_env = run()
+    assert np.array_equal(S_cc, S_env) and np.array_equal(d_cc, d_env)
+    for S, dX in ((S_cc, d_cc), (S_tc, d_tc)):
+        assert ora.rel_err(S, ref) <= TOL32
+        assert ora.rel_err(dX, dref) <= TOL32
