@@ -254,9 +254,9 @@ def cpu_threads() -> int:
 
 
 def workload(name: str, precision: str = "config"):
-    from tests.configs import CONFIGS
+    from tests.configs import ALL_CONFIGS
 
-    cfg = dict(CONFIGS[name])
+    cfg = dict(ALL_CONFIGS[name])
     if precision == "fp64":
         cfg["dtype"] = np.float64
     return cfg

@@ -119,6 +119,10 @@ struct JitPlan {
   void* kern[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   bool failed[2][2] = {{false, false}, {false, false}};
   bool broken = false;  // some compilation failed: route this plan elsewhere
+  // the fragment kernels served a call while the cubin compiled: this plan keeps serving that
+  // [dtype][direction] with them, so its results stay bitwise reproducible call to call (the
+  // reference's determinism contract); the cubin lands in the cache for later plans / processes
+  bool standin[2][2] = {{false, false}, {false, false}};
   std::shared_ptr<jit::Pending> pending[2][2];  // background compiles in flight / finished
   std::mutex mu;                                // guards the compile / load state above
 };
@@ -128,8 +132,9 @@ void make_plan(const Trie& t, JitHost& h);
 std::string source(const Trie& t, const JitHost& h, int dtype, bool backward);
 // Compile / load the generated kernel.  A cubin-cache hit loads at once; otherwise,
 // unless `wait`, the NVRTC compile runs on a background host thread and ensure
-// returns kPending (the caller serves the call with the fragment kernels) until
-// the cubin is ready.  SIGB_OK when the kernel is loaded, else an error code.
+// returns kPending (the caller serves the call with the fragment kernels) -- from then
+// on for this plan, dtype and direction (JitPlan::standin).  SIGB_OK when the kernel is
+// loaded, else an error code.
 constexpr int kPending = -1;
 int ensure(sigb_plan* p, int dtype, bool backward, bool wait);
 bool wait_default();  // policy 4 or SIGB_JIT_SYNC=1: compile synchronously

@@ -843,6 +843,7 @@ int ensure(sigb_plan* p, int dtype, bool backward, bool wait) {
   const int di = dtype == SIGB_F32 ? 0 : 1, bi = backward ? 1 : 0;
   std::lock_guard<std::mutex> lock(J.mu);
   if (J.kern[di][bi]) return SIGB_OK;
+  if (J.standin[di][bi]) return kPending;
   if (J.failed[di][bi]) return fail(SIGB_ERR_UNSUPPORTED, "word-set kernel compilation failed earlier");
   std::shared_ptr<Pending>& pd = J.pending[di][bi];
   if (!pd) {
@@ -869,7 +870,10 @@ int ensure(sigb_plan* p, int dtype, bool backward, bool wait) {
   if (wait)
     while (pd->state.load(std::memory_order_acquire) == 0) std::this_thread::sleep_for(std::chrono::milliseconds(5));
   const int st = pd->state.load(std::memory_order_acquire);
-  if (st == 0) return kPending;
+  if (st == 0) {
+    J.standin[di][bi] = true;
+    return kPending;
+  }
   if (st == 2) {
     J.failed[di][bi] = J.broken = true;
     return fail(SIGB_ERR_UNSUPPORTED, pd->err);

@@ -30,7 +30,7 @@ PAPER_CONFIGS = {
     "p2": dict(seed=12, kind="truncated", d=10, depth=4, B=256, L=201, dtype=np.float32, bwd=True,
                paper_ms=9.83, paper_row="(256, 200, 10) N=4: pathsig 9.83 ms on H200"),
 }
-CONFIGS.update(PAPER_CONFIGS)
+ALL_CONFIGS = {**CONFIGS, **PAPER_CONFIGS}
 
 
 def brownian(seed: int, B: int, L: int, d: int, chunk: int | None = None) -> np.ndarray:
@@ -76,7 +76,7 @@ def c3_words() -> list[tuple[int, ...]]:
 
 def build_wordset(name: str, sk):
     """Build config `name`'s word set with module `sk` (this package or sigkit)."""
-    cfg = CONFIGS[name]
+    cfg = ALL_CONFIGS[name]
     if cfg["kind"] == "truncated":
         return sk.build_truncated(cfg["d"], cfg["depth"])
     if cfg["kind"] == "custom":
