@@ -120,6 +120,10 @@ int64_t sigb_plan_closure_size(const sigb_plan* plan);
 int64_t sigb_plan_num_parts(const sigb_plan* plan);
 /* Executed FMA count of one Chen step of one path (T-node count; diagnostics). */
 int64_t sigb_plan_step_fmas(const sigb_plan* plan);
+/* Thread blocks the forward launches for B whole paths on this plan's register-resident
+ * truncated kernels (-1 for other kernel families): the host side's fill measure for the
+ * parallel-in-time route of small batches (signature.py _scan_forward). */
+int64_t sigb_forward_ctas(const sigb_plan* plan, int64_t B);
 /* Kernel family sigb_forward / sigb_backward will run for this plan under the
  * current policy: 1 = register-resident truncated kernels, 2 = register-resident
  * fragment kernels (any trie), 4 = word-set-specialised generated kernels (small sparse sets),

@@ -40,6 +40,7 @@ SIGNATURES = {
     "sigb_device_sm_count": (ctypes.c_int, []),
     "sigb_set_kernel_policy": (_C, [_C]),
     "sigb_set_tensor_cores": (_C, [_C]),
+    "sigb_forward_ctas": (_I, [_P, _I]),
     "sigb_launch_count": (ctypes.c_longlong, []),
     "sigb_timing_enable": (_C, [_C]),
     "sigb_timing_read": (_C, [_C, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I)]),

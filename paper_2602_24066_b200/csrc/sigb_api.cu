@@ -201,6 +201,10 @@ extern "C" int sigb_set_kernel_policy(int policy) {
   g_policy = policy;
   return SIGB_OK;
 }
+extern "C" int64_t sigb_forward_ctas(const sigb_plan* plan, int64_t B) {
+  if (!plan || B < 0) return -1;
+  return use_trunc(plan) ? trunc::forward_ctas(plan->d, plan->trunc_depth, B) : -1;
+}
 extern "C" int sigb_set_tensor_cores(int on) {
   const int prev = g_tensor_cores;
   g_tensor_cores = on ? 1 : 0;

@@ -231,6 +231,7 @@ int backward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L,
 }  // namespace frag
 namespace trunc {
 bool supported(int64_t d, int depth);
+int64_t forward_ctas(int64_t d, int depth, int64_t B);  // grid of the truncated forward for B paths
 int forward(int dtype, int64_t d, int depth, const void* X, int64_t B, int64_t L, const int64_t* bounds, int64_t K,
             void* out, int64_t out_ld, int64_t out_col0, int include_empty, cudaStream_t stream);
 // stride > 0: the reference's checkpoint_stride (backward.py:183-199): a forward replay stores the

@@ -191,6 +191,17 @@ int bwd(const T* X, int64_t B, int64_t L, const T* S, int64_t s_ld, int64_t s_co
 
 }  // namespace
 
+int64_t forward_ctas(int64_t d, int depth, int64_t B) {
+#define X(D_, N_, GF_, GB_)                                                      \
+  if (d == D_ && depth == N_) {                                                  \
+    using C = Cfg<D_, N_, GF_>;                                                  \
+    return C::CPP > 1 ? B * C::CPP : (B + C::PPC - 1) / C::PPC;                  \
+  }
+  SIGB_TRUNC_CASES(X)
+#undef X
+  return -1;
+}
+
 bool supported(int64_t d, int depth) {
 #define X(D_, N_, GF_, GB_) \
   if (d == D_ && depth == N_) return true;

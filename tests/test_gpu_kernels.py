@@ -281,3 +281,33 @@ def test_generated_kernels_many_path_blocks(d, misaligned):
         assert ora.rel_err(sk.signature_backward(X, ws, g).path_grads, dref) <= TOL64
     finally:
         _lib.set_kernel_policy(0)
+
+
+@pytest.mark.parametrize("d,N,B,L,force", [(4, 4, 4, 5001, False), (4, 6, 2, 4101, False), (8, 4, 5, 300, True),
+                                            (16, 4, 3, 200, True), (4, 4, 32, 128, True)])
+def test_parallel_in_time_forward(d, N, B, L, force, monkeypatch):
+    """Small batches of long paths on full truncations run as T windows per path joined by a
+    tree of truncated tensor products (signature.py _scan_forward; Chen's identity, reference
+    sigcore.py:321-334): same values as the oracle (fp64 1e-10, fp32 1e-4) and as the
+    sequential sweep (SIGB_SCAN=0), bitwise reproducible."""
+    from paper_2602_24066_b200.signature import _scan_segments
+
+    if force:
+        monkeypatch.setenv("SIGB_SCAN", "2")
+    ws = sk.build_truncated(d, N)
+    X = brownian(60 + d, B, L, d)
+    assert _scan_segments(ws.plan(), ws, B, L - 1) > 1
+    ref = ora.forward(X, ws.codes, ws.lengths, d)
+    out = sk.signature_forward(X, ws).values
+    assert ora.rel_err(out, ref) <= TOL64
+    assert np.array_equal(out, sk.signature_forward(X, ws).values)
+    X32 = X.astype(np.float32)
+    out32 = sk.signature_forward(X32, ws).values
+    ref32 = ora.forward(X32.astype(np.float64), ws.codes, ws.lengths, d)
+    assert ora.rel_err(out32, ref32) <= TOL32
+    monkeypatch.setenv("SIGB_SCAN", "0")
+    assert ora.rel_err(sk.signature_forward(X, ws).values, out) <= TOL64
+    ws_e = sk.build_truncated(d, N, include_empty=True)
+    monkeypatch.setenv("SIGB_SCAN", "2" if force else "1")
+    oe = sk.signature_forward(X, ws_e).values
+    assert np.all(oe[:, 0] == 1.0) and ora.rel_err(oe[:, 1:], ref) <= TOL64
