@@ -77,7 +77,7 @@ def parse_args(argv=None):
     p.add_argument("--weak", action="store_true", help="every rank runs the config's whole batch (weak scaling)")
     p.add_argument("--strong", action="store_true", help="(default) shard one fixed global batch across the ranks")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--e2e-split", type=int, default=4, help="sub-batches per e2e step (copy/compute pipeline)")
+    p.add_argument("--e2e-split", type=int, default=8, help="sub-batches per e2e step (copy/compute pipeline)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--gather", action="store_true", help="also time the optional NCCL all-gather of S")
     p.add_argument("--policy", type=int, default=0, help="0 auto kernels, 1 generic trie kernels only")

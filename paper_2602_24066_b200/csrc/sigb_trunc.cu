@@ -86,27 +86,37 @@ size_t bwd_workspace(int64_t B, int64_t L, int64_t stride = 0) {
          ((size_t)C::CPP * (L - 1) * D + ckpt_words<D, N, G>(L, stride));
 }
 
+// dL/dX from the per-part partials: dInc_j = sum_p partial[p][j] (parts in ascending order), then
+// the telescoping dX_0 = -dInc_0, dX_t = dInc_{t-1} - dInc_t, dX_M = dInc_{M-1} (backward.py:130-147).
+// A thread walks kSeg consecutive samples of one (path, channel), so each dInc is summed once
+// (the per-sample form summed every increment twice); same arithmetic, same bits.
+constexpr int kSeg = 32;
 template <typename T>
 __global__ void trunc_sample_grads(const T* __restrict__ partial, int64_t Bc, int64_t P, int64_t M, int64_t d,
                                    int64_t b0, int64_t B, T* __restrict__ dX, T* __restrict__ dinc) {
-  const int64_t L = M + 1;
+  const int64_t L = M + 1, nseg = (L + kSeg - 1) / kSeg;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= Bc * L * d) return;
-  const int64_t z = i % d, t = (i / d) % L, bl = i / (d * L);
+  if (i >= Bc * nseg * d) return;
+  const int64_t z = i % d, sg = (i / d) % nseg, bl = i / (d * nseg);
   if (b0 + bl >= B) return;
   auto inc = [&](int64_t j) {
     T s = T(0);
     for (int64_t p = 0; p < P; ++p) s += partial[((bl * P + p) * M + j) * d + z];
     return s;
   };
-  T v = T(0);
-  if (t >= 1) v += inc(t - 1);
-  if (t < M) {
-    const T it = inc(t);
-    v -= it;
-    if (dinc) dinc[((b0 + bl) * M + t) * d + z] = it;
+  const int64_t t0 = sg * kSeg, t1 = t0 + kSeg < L ? t0 + kSeg : L;
+  T prev = t0 >= 1 ? inc(t0 - 1) : T(0);
+  for (int64_t t = t0; t < t1; ++t) {
+    T v = T(0);
+    if (t >= 1) v += prev;
+    if (t < M) {
+      const T it = inc(t);
+      v -= it;
+      if (dinc) dinc[((b0 + bl) * M + t) * d + z] = it;
+      prev = it;
+    }
+    dX[((b0 + bl) * L + t) * d + z] = v;
   }
-  dX[((b0 + bl) * L + t) * d + z] = v;
 }
 
 template <typename T, int D, int N, int G>
@@ -168,7 +178,7 @@ int bwd(const T* X, int64_t B, int64_t L, const T* S, int64_t s_ld, int64_t s_co
     }
     timing_end(1, stream);
     SIGB_CUDA_TRY(cudaGetLastError());
-    const int64_t n = Bc * L * D;
+    const int64_t n = Bc * ((L + kSeg - 1) / kSeg) * D;
     trunc_sample_grads<T><<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(partial, Bc, C::CPP, M, D, b0, B, dX,
                                                                            dinc);
     SIGB_CUDA_TRY(cudaGetLastError());
