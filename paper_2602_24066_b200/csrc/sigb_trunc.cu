@@ -135,21 +135,26 @@ int bwd(const T* X, int64_t B, int64_t L, const T* S, int64_t s_ld, int64_t s_co
   auto kern = stride > 0 ? (async ? trunc_backward_kernel<T, D, N, G, true, false, true>
                                   : trunc_backward_kernel<T, D, N, G, false, false, true>)
                          : (async ? trunc_backward_kernel<T, D, N, G, true> : trunc_backward_kernel<T, D, N, G, false>);
+  // leaf level on the tensor cores (fp32, d = 16 depth 4 and d = 8 depth 5).  SIGB_TRUNC_TC_BWD
+  // selects: 2 (default) the P/Q kernel (sigb_trunc_pq.cuh, both leaf sums on tcgen05), 1 the
+  // parent pull-back only on tcgen05 (TcBwd, d = 16 only), 0 the CUDA-core kernel (A/B
+  // experiments, parity tests); checkpoints and sigb_set_tensor_cores(0) take the CUDA cores
+  constexpr bool kPQ = std::is_same<T, float>::value && ((D == 16 && N == 4) || (D == 8 && N == 5));
   bool pq_kernel = false;
-  if constexpr (std::is_same<T, float>::value && D == 16 && N == 4 && G == 4) {
-    // leaf level on the tensor cores.  SIGB_TRUNC_TC_BWD selects: 2 (default) the P/Q kernel
-    // (sigb_trunc_pq.cuh, both leaf sums on tcgen05), 1 the parent pull-back only on tcgen05
-    // (TcBwd), 0 the CUDA-core kernel (A/B experiments, parity tests)
+  if constexpr (kPQ) {
     const char* e = getenv("SIGB_TRUNC_TC_BWD");
-    const int mode = (stride > 0 || !g_tensor_cores) ? 0 : (e ? atoi(e) : 2);  // checkpoints: CUDA-core kernel
-    if (mode == 2 && force_async != 0) {
+    const int mode = (stride > 0 || !g_tensor_cores) ? 0 : (e ? atoi(e) : 2);
+    if (mode == 2) {
+      static_assert(pq::PQ<D, N>::CPP == C::CPP, "the P/Q kernel fills the same partial layout");
       pq_kernel = true;
-      smem = pq::kSmem;
-      SIGB_CUDA_TRY(cudaFuncSetAttribute(pq::trunc_pq_backward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
-    } else if (mode == 1 && force_async != 0) {
-      kern = trunc_backward_kernel<T, D, N, G, true, true>;
-      smem += TcBwd::bytes;
+      smem = pq::PQ<D, N>::kSmem;
+      SIGB_CUDA_TRY(cudaFuncSetAttribute(pq::trunc_pq_backward_kernel<D, N>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    } else if constexpr (D == 16 && G == 4) {
+      if (mode == 1 && force_async != 0) {
+        kern = trunc_backward_kernel<T, D, N, G, true, true>;
+        smem += TcBwd::bytes;
+      }
     }
   }
   if (!pq_kernel) SIGB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -165,10 +170,10 @@ int bwd(const T* X, int64_t B, int64_t L, const T* S, int64_t s_ld, int64_t s_co
     }
     count_launch(2);
     timing_begin(1, stream);
-    if constexpr (std::is_same<T, float>::value && D == 16 && N == 4 && G == 4) {
+    if constexpr (kPQ) {
       if (pq_kernel)
-        pq::trunc_pq_backward_kernel<<<(unsigned)grid, pq::kBlock, smem, stream>>>(X, B, L, b0, S, s_ld, s_col0, g,
-                                                                                     g_ld, g_col0, partial);
+        pq::trunc_pq_backward_kernel<D, N><<<(unsigned)grid, pq::kBlock, smem, stream>>>(X, B, L, b0, S, s_ld, s_col0,
+                                                                                           g, g_ld, g_col0, partial);
       else
         kern<<<(unsigned)grid, C::THREADS, smem, stream>>>(X, B, L, b0, S, s_ld, s_col0, g, g_ld, g_col0, partial,
                                                            ckpt, stride);

@@ -50,36 +50,41 @@ namespace sigb {
 namespace trunc {
 namespace pq {
 
-constexpr int D = 16;
-constexpr int kThreads = 256;  // compute threads: a quarter path
+// Geometry shared by the instantiations (d = 16, depth 4: config 5; d = 8, depth 5: config 2):
+// a CTA holds 1,024 leaf parents (four per compute thread), i.e. a quarter path in both.
+constexpr int kThreads = 256;          // compute threads
 constexpr int kBlock = kThreads + 32;  // + the producer warp
-constexpr int CPP = 4;         // CTAs per path
-constexpr int CH = 32;         // steps per chunk
-constexpr int NG = 16;         // steps per MMA group (MMA N)
-constexpr int kTiles = 8;      // 1,024 rows per operand / 128
-constexpr int kRowHalves = 128 * 16;
+constexpr int CH = 32;                 // steps per chunk
+constexpr int NG = 16;                 // steps per MMA group (MMA N)
+constexpr int kTiles = 8;              // 1,024 rows per operand / 128
+constexpr int kRowHalves = 128 * 16;   // one A tile: 128 rows x K = 16 fp16 (d < 16 pads with zeros)
 constexpr int kAHalves = kTiles * kRowHalves;
 
-// shared memory (bytes); B, increments, parked sums and 1/sigma are double-buffered by chunk parity
-constexpr int oA1h = 0, oA1l = oA1h + 2 * kAHalves, oA2h = oA1l + 2 * kAHalves, oA2l = oA2h + 2 * kAHalves;
-constexpr int kBBytes = 2 * CH * 16;                   // one of hi / lo
-constexpr int oB = oA2l + 2 * kAHalves;                // [2 buffers][hi, lo]
-constexpr int oXs = oB + 2 * 2 * kBBytes;              // two sample buffers (CH + 1) x D
-constexpr int oDl = oXs + 2 * 4 * (CH + 1) * D;        // [2][CH][D] increments
-constexpr int oRed = oDl + 2 * 4 * CH * D;             // [2][8 warps][CH][D] per-warp letter sums
-constexpr int oSig = oRed + 2 * 4 * 8 * CH * D;        // [2][CH] 1 / sigma per step
-constexpr int oBar = oSig + 2 * 4 * CH;                // mbarriers: MMA group 0, 1; increments ready 0, 1
-constexpr int oSlot = oBar + 32;
-constexpr size_t kSmem = oSlot + 16;
+template <int D, int N>
+struct PQ {
+  static_assert(D == 16 || D == 8, "letter quads: d = 8 or 16");
+  static constexpr int QPG = D / 4;                    // threads per grand-parent (letter quads)
+  static constexpr int GPC = kThreads / QPG;           // grand-parents per CTA
+  static constexpr int NGP = trunc::ipow(D, N - 2);    // grand-parents per path
+  static constexpr int CPP = NGP / GPC;                // CTAs per path
+  static constexpr int NC = N - 2;                     // chain nodes (levels 1 .. N-2)
+  static_assert(GPC * D == 1024 && NGP % GPC == 0, "1,024 leaf parents per CTA");
+  // canonical word offsets of a full truncation: level l starts at sum_{k<l} D^k
+  __host__ __device__ static constexpr int64_t off(int l) { return trunc::Cfg<D, N, 4>::off(l); }
+  // shared memory (bytes); B, increments, parked sums and 1/sigma are double-buffered by chunk parity
+  static constexpr int oA1h = 0, oA1l = oA1h + 2 * kAHalves, oA2h = oA1l + 2 * kAHalves;
+  static constexpr int oA2l = oA2h + 2 * kAHalves;
+  static constexpr int kBBytes = 2 * CH * 16;            // one of hi / lo
+  static constexpr int oB = oA2l + 2 * kAHalves;         // [2 buffers][hi, lo]
+  static constexpr int oXs = oB + 2 * 2 * kBBytes;       // two sample buffers (CH + 1) x D
+  static constexpr int oDl = oXs + 2 * 4 * (CH + 1) * D; // [2][CH][D] increments
+  static constexpr int oRed = oDl + 2 * 4 * CH * D;      // [2][8 warps][CH][D] per-warp letter sums
+  static constexpr int oSig = oRed + 2 * 4 * 8 * CH * D; // [2][CH] 1 / sigma per step
+  static constexpr int oBar = oSig + 2 * 4 * CH;         // mbarriers: MMA group 0, 1; increments ready 0, 1
+  static constexpr int oSlot = oBar + 32;
+  static constexpr size_t kSmem = oSlot + 16;
+};
 
-// canonical word indices of a full truncation d = 16: levels start at 0, 16, 272, 4368
-__device__ __forceinline__ int idx2(int gp) { return 16 + gp; }
-__device__ __forceinline__ int idx3(int gp, int y) { return 272 + gp * 16 + y; }
-__device__ __forceinline__ int idx4(int gp, int y, int z) { return 4368 + (gp * 16 + y) * 16 + z; }
-
-// wait for this thread's outstanding tcgen05.ld; the "+r" operands order every use of the loaded
-// registers after the wait, and there is no memory clobber, so shared-memory traffic of the
-// neighbouring steps may move across it (the two unrolled steps interleave)
 __device__ __forceinline__ void ld_wait8(uint32_t (&r)[8]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;"
                : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]));
@@ -90,32 +95,46 @@ __device__ __forceinline__ void ld_wait16(uint32_t (&a)[8], uint32_t (&b)[8]) {
                  "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]), "+r"(b[6]), "+r"(b[7]));
 }
 
+template <int D, int N>
 __global__ void __launch_bounds__(kBlock, 1)
     trunc_pq_backward_kernel(const float* __restrict__ X, int64_t B, int64_t L, int64_t b0,
                              const float* __restrict__ Sin, int64_t s_ld, int64_t s_col0,
                              const float* __restrict__ gup, int64_t g_ld, int64_t g_col0,
                              float* __restrict__ partial) {
+  using Q_ = PQ<D, N>;
+  constexpr int QPG = Q_::QPG, GPC = Q_::GPC, CPP = Q_::CPP, NC = Q_::NC;
   extern __shared__ __align__(1024) unsigned char sm[];
-  __half* A1h = reinterpret_cast<__half*>(sm + oA1h);
-  __half* A1l = reinterpret_cast<__half*>(sm + oA1l);
-  __half* A2h = reinterpret_cast<__half*>(sm + oA2h);
-  __half* A2l = reinterpret_cast<__half*>(sm + oA2l);
-  auto Bhi = [&](int db) { return reinterpret_cast<__half*>(sm + oB + db * 2 * kBBytes); };
-  auto Blo = [&](int db) { return reinterpret_cast<__half*>(sm + oB + db * 2 * kBBytes + kBBytes); };
-  auto Xsb = [&](int db) { return reinterpret_cast<float*>(sm + oXs) + db * (CH + 1) * D; };
-  auto Dlb = [&](int db) { return reinterpret_cast<float*>(sm + oDl) + db * CH * D; };
-  float(*red)[8][CH][D] = reinterpret_cast<float(*)[8][CH][D]>(sm + oRed);
-  auto isig = [&](int db) { return reinterpret_cast<float*>(sm + oSig) + db * CH; };
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + oBar);
-  uint32_t* slot = reinterpret_cast<uint32_t*>(sm + oSlot);
+  __half* A1h = reinterpret_cast<__half*>(sm + Q_::oA1h);
+  __half* A1l = reinterpret_cast<__half*>(sm + Q_::oA1l);
+  __half* A2h = reinterpret_cast<__half*>(sm + Q_::oA2h);
+  __half* A2l = reinterpret_cast<__half*>(sm + Q_::oA2l);
+  auto Bhi = [&](int db) { return reinterpret_cast<__half*>(sm + Q_::oB + db * 2 * Q_::kBBytes); };
+  auto Blo = [&](int db) { return reinterpret_cast<__half*>(sm + Q_::oB + db * 2 * Q_::kBBytes + Q_::kBBytes); };
+  auto Xsb = [&](int db) { return reinterpret_cast<float*>(sm + Q_::oXs) + db * (CH + 1) * D; };
+  auto Dlb = [&](int db) { return reinterpret_cast<float*>(sm + Q_::oDl) + db * CH * D; };
+  float(*red)[8][CH][D] = reinterpret_cast<float(*)[8][CH][D]>(sm + Q_::oRed);
+  auto isig = [&](int db) { return reinterpret_cast<float*>(sm + Q_::oSig) + db * CH; };
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + Q_::oBar);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(sm + Q_::oSlot);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool producer = warp == kThreads / 32;
   const int64_t b = b0 + blockIdx.x / CPP;  // the grid covers live paths only
   const int cip = blockIdx.x % CPP;
-  const int q = lane & 3;
-  const int gp = ((cip * kThreads + tid) >> 2) & 255;  // 0..255 (the producer warp's value is unused)
-  const int la = gp >> 4, lb = gp & 15;       // letters of the chain: node la (level 1), node gp (level 2)
+  const int q = lane & (QPG - 1);  // letter quad
+  // grand-parent (level N-2 word, 0 .. D^(N-2)-1); the producer warp's value is unused but valid
+  const int gp = ((cip * kThreads + tid) / QPG) % Q_::NGP;
+  int cl[NC];  // the chain's letters: node k (level k+1) ends with letter cl[k]
+  {
+    int code = gp;
+#pragma unroll
+    for (int k = NC - 1; k >= 0; --k) {
+      cl[k] = code % D;
+      code /= D;
+    }
+  }
+  auto chain_index = [&](int k) { return Q_::off(k + 1) + gp / trunc::ipow(D, NC - 1 - k); };
+  auto par_index = [&](int y) { return Q_::off(N - 1) + (int64_t)gp * D + y; };
   const int64_t M = L - 1;
   const int r = 32 * (warp & 3) + lane;       // this thread's row in every tile = its TMEM lane
   const int mt0 = (warp >> 2) * 4;            // its tiles mt0 .. mt0 + 3
@@ -132,39 +151,43 @@ __global__ void __launch_bounds__(kBlock, 1)
   }
 
   // ---- terminal state, adjoint seeds, P, and the constant A operands ----
-  // The CTA's 16,384 leaf adjoints (contiguous in the upstream row: leaves of grand-parents
-  // 64 cip .. 64 cip + 63) and 1,024 parent values are staged in shared memory first (all 288
-  // threads, coalesced cp.async; the A2 region and the parked-sums region are free until the
-  // sweep), so each thread reads its A1 rows / A2 columns / P terms from shared memory.
+  // The CTA's 1,024 x D leaf adjoints (contiguous in the upstream row: the leaves of its GPC
+  // grand-parents) and 1,024 parent values are staged in shared memory first (all 288 threads,
+  // coalesced cp.async; the A2 region and the parked-sums region are free until the sweep), so
+  // each thread reads its A1 rows / A2 columns / P terms from shared memory.
   const float* srow = Sin + b * s_ld + s_col0;
   const float* grow = gup + b * g_ld + g_col0;
-  float* lstage = reinterpret_cast<float*>(sm + oA2h);  // [64 gp][16 y][16 z] fp32 (64 KB = A2 hi + lo)
-  float* sstage = reinterpret_cast<float*>(sm + oRed);  // [64 gp][16 y] parent values
+  float* lstage = reinterpret_cast<float*>(sm + Q_::oA2h);  // [GPC][D y][D z] fp32 (<= 64 KB = A2 hi + lo)
+  float* sstage = reinterpret_cast<float*>(sm + Q_::oRed);  // [GPC][D y] parent values
   {
-    const float* lsrc = grow + idx4(64 * cip, 0, 0);
-    for (int i = tid; i < 64 * 256; i += kBlock)
+    const float* lsrc = grow + Q_::off(N) + (int64_t)cip * GPC * D * D;
+    for (int i = tid; i < GPC * D * D; i += kBlock)
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tcu::su32(lstage + i)), "l"(lsrc + i) : "memory");
-    const float* ssrc = srow + idx3(64 * cip, 0);
-    for (int i = tid; i < 64 * 16; i += kBlock)
+    const float* ssrc = srow + Q_::off(N - 1) + (int64_t)cip * GPC * D;
+    for (int i = tid; i < GPC * D; i += kBlock)
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tcu::su32(sstage + i)), "l"(ssrc + i) : "memory");
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  float sc0 = srow[la], sc1 = srow[idx2(gp)];
-  float lc0 = (q == 0 && lb == 0) ? grow[la] : 0.f;  // seeded once per chain node
-  float lc1 = q == 0 ? grow[idx2(gp)] : 0.f;
+  float sc[NC], lc[NC];  // chain values S_j and (partial) adjoints; a node is seeded once (the owner)
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    sc[k] = srow[chain_index(k)];
+    const bool owner = q == 0 && gp % trunc::ipow(D, NC - 1 - k) == 0;
+    lc[k] = owner ? grow[chain_index(k)] : 0.f;
+  }
   float lm_[4], P[4] = {0.f, 0.f, 0.f, 0.f};  // (the P/Q form never reads the parents' S_j)
 #pragma unroll
-  for (int g = 0; g < 4; ++g) lm_[g] = grow[idx3(gp, 4 * q + g)];
+  for (int g = 0; g < 4; ++g) lm_[g] = grow[par_index(4 * q + g)];
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
-  const int gl_ = (gp - 64 * cip) & 63;  // grand-parent within the CTA (the producer warp reads a valid one)
-  const float* lg = lstage + gl_ * 256;
-  float a2v[4][16];  // Lambda[gp, y, 4q + i]: this thread's A2 rows (held across the barrier below)
+  const int gl_ = (gp - GPC * cip) & (GPC - 1);  // grand-parent within the CTA (valid for the producer too)
+  const float* lg = lstage + gl_ * D * D;
+  float a2v[4][D];  // Lambda[gp, y, 4q + i]: this thread's A2 rows (held across the barrier below)
   float amax1 = 0.f, amax2 = 0.f;
 #pragma unroll
-  for (int y = 0; y < 16; ++y) {
-    const float sy = sstage[gl_ * 16 + y];
-    const float4 l4 = *reinterpret_cast<const float4*>(lg + y * 16 + 4 * q);
+  for (int y = 0; y < D; ++y) {
+    const float sy = sstage[gl_ * D + y];
+    const float4 l4 = *reinterpret_cast<const float4*>(lg + y * D + 4 * q);
     a2v[0][y] = l4.x; a2v[1][y] = l4.y; a2v[2][y] = l4.z; a2v[3][y] = l4.w;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -175,17 +198,17 @@ __global__ void __launch_bounds__(kBlock, 1)
 #pragma unroll
   for (int g = 0; g < 4; ++g)
 #pragma unroll
-    for (int z = 0; z < 16; ++z) amax1 = fmaxf(amax1, fabsf(lg[(4 * q + g) * 16 + z]));
+    for (int z = 0; z < D; ++z) amax1 = fmaxf(amax1, fabsf(lg[(4 * q + g) * D + z]));
   const float s1 = tcu::pow2_scale(amax1), s2 = tcu::pow2_scale(amax2);
   const float inv_s1 = 1.f / s1, inv_s2 = 1.f / s2;  // exact: powers of two
   if (!producer) {
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {  // A1 row (tile mt0 + g) = parent gp.(4q+g), K = leaf letter z
+    for (int g = 0; g < 4; ++g) {  // A1 row (tile mt0 + g) = parent gp.(4q+g), K = leaf letter z (zero-padded)
 #pragma unroll
       for (int kg = 0; kg < 2; ++kg) {
         float v[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = lg[(4 * q + g) * 16 + 8 * kg + i];
+        for (int i = 0; i < 8; ++i) v[i] = 8 * kg + i < D ? lg[(4 * q + g) * D + 8 * kg + i] : 0.f;
         const int off = (mt0 + g) * kRowHalves + tcu::kmajor_off16<2>(r, 8 * kg);
         tcu::split8_store(v, s1, A1h + off, A1l + off);
       }
@@ -194,12 +217,12 @@ __global__ void __launch_bounds__(kBlock, 1)
   __syncthreads();  // the staged leaf adjoints are read: their region becomes A2
   if (!producer) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {  // A2 row (tile mt0 + i) = pair (gp, 4q+i), K = parent letter y
+    for (int i = 0; i < 4; ++i) {  // A2 row (tile mt0 + i) = pair (gp, 4q+i), K = parent letter y (zero-padded)
 #pragma unroll
       for (int kg = 0; kg < 2; ++kg) {
         float v[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = a2v[i][8 * kg + k];
+        for (int k = 0; k < 8; ++k) v[k] = 8 * kg + k < D ? a2v[i][(8 * kg + k) % D] : 0.f;
         const int off = (mt0 + i) * kRowHalves + tcu::kmajor_off16<2>(r, 8 * kg);
         tcu::split8_store(v, s2, A2h + off, A2l + off);
       }
@@ -210,14 +233,15 @@ __global__ void __launch_bounds__(kBlock, 1)
   __syncthreads();
   tcu::fence_after();
   const uint32_t tmem = *slot;
-  // chain letters' home lanes: ma / mb select v[la & 3] at q == la / 4 (resp. lb)
-  float ma[4], mb[4];
+  // chain letters' home lanes: mk[k][i] selects slot i (letter 4q+i) of the lane whose quad holds cl[k]
+  float mk[NC][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    ma[i] = (q == (la >> 2) && i == (la & 3)) ? 1.f : 0.f;
-    mb[i] = (q == (lb >> 2) && i == (lb & 3)) ? 1.f : 0.f;
-  }
+  for (int k = 0; k < NC; ++k)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) mk[k][i] = (q == (cl[k] >> 2) && i == (cl[k] & 3)) ? 1.f : 0.f;
   const int my_letter = 4 * q + ((lane & 16) ? 2 : 0) + ((lane & 8) ? 1 : 0);
+  // lanes summed plainly in the letter reduction (the grand-parent bits below bit 3)
+  constexpr int kPlainMask = (8 - 1) & ~(QPG - 1);
 
   // ---- chunk pipeline (chunk k = the k-th processed, c = nchunks-1-k; buffers by k & 1).
   // The producer warp stages samples two chunks ahead (cp.async), forms increments, B and
@@ -245,7 +269,7 @@ __global__ void __launch_bounds__(kBlock, 1)
     __syncwarp();
     float v[16];  // lane = step row of B; rows past the chunk are zero
 #pragma unroll
-    for (int z = 0; z < 16; ++z) v[z] = lane < cs ? dl[lane * D + z] : 0.f;
+    for (int z = 0; z < 16; ++z) v[z] = (lane < cs && z < D) ? dl[lane * D + (z % D)] : 0.f;
     float amax = 0.f;
 #pragma unroll
     for (int z = 0; z < 16; ++z) amax = fmaxf(amax, fabsf(v[z]));
@@ -288,33 +312,36 @@ __global__ void __launch_bounds__(kBlock, 1)
   // ahead so the next step's shared loads sit above this step's parked-sum store
   struct Inc {
     float4 y;
-    float d0, d1, is;
+    float dc[NC];
+    float is;
   };
   auto fetch = [&](int s, const float* dl, const float* isg) {
     const float* row = dl + s * D;
     Inc in;
     in.y = *reinterpret_cast<const float4*>(row + 4 * q);
-    in.d0 = row[la];
-    in.d1 = row[lb];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) in.dc[k] = row[cl[k]];
     in.is = isg[s];
     return in;
   };
   // a step's letter sums before the cross-lane reduction: the reduction of step s is issued after
   // the arithmetic of step s-1 (source order), so its shuffle latency overlaps that arithmetic
   struct Sums {
-    float v[4], gc0, gc1;
+    float v[4], gc[NC];
   };
   auto reduce = [&](Sums& u, int s, float(*redw)[D]) {
-    float gc0 = u.gc0, gc1 = u.gc1;
     float* v = u.v;
-    // the quad's partial chain terms -> full per grand-parent, added at the lane of their letter
-    gc0 += __shfl_xor_sync(0xffffffffu, gc0, 1);
-    gc1 += __shfl_xor_sync(0xffffffffu, gc1, 1);
-    gc0 += __shfl_xor_sync(0xffffffffu, gc0, 2);
-    gc1 += __shfl_xor_sync(0xffffffffu, gc1, 2);
+    // the quad group's partial chain terms -> full per grand-parent, added at the lane of their letter
 #pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = fmaf(ma[i], gc0, fmaf(mb[i], gc1, v[i]));
-    // sum over the warp's 8 grand-parents (lane bits 4, 3, 2): transposing, one letter per lane pair
+    for (int msk = 1; msk < QPG; msk *= 2)
+#pragma unroll
+      for (int k = 0; k < NC; ++k) u.gc[k] += __shfl_xor_sync(0xffffffffu, u.gc[k], msk);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int k = 0; k < NC; ++k) v[i] = fmaf(mk[k][i], u.gc[k], v[i]);
+    // sum over the warp's grand-parents: transposing over lane bits 4 and 3 (one letter per lane
+    // group), plain over the grand-parent bits below
     const bool u4 = (lane & 16) != 0, u3 = (lane & 8) != 0;
     {
       const float s0 = u4 ? v[0] : v[2], s1v = u4 ? v[1] : v[3];
@@ -326,56 +353,114 @@ __global__ void __launch_bounds__(kBlock, 1)
       const float snd = u3 ? v[0] : v[1], kp = u3 ? v[1] : v[0];
       v[0] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
     }
-    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 4);
-    if ((lane & 4) == 0) redw[s][my_letter] = v[0];
+#pragma unroll
+    for (int msk = 4; msk >= QPG; msk /= 2) v[0] += __shfl_xor_sync(0xffffffffu, v[0], msk);
+    if ((lane & kPlainMask) == 0) redw[s][my_letter] = v[0];
   };
   auto step = [&](const Inc& in, const uint32_t (&rr)[8]) -> Sums {
     const float dy[4] = {in.y.x, in.y.y, in.y.z, in.y.w};
-    const float d0 = in.d0, d1 = in.d1, is = in.is;
-    // (a) reconstruct S_j = S_{j+1} (x) exp(-dX_j) on the chain and the parents
-    const float r0_3 = sc0 - d0 * (1.f / 3.f);
-    const float tr3 = fmaf(-0.5f * d1, r0_3, sc1);  // Tr(gp, 3): the exp(-dX) partial
-    const float nsc1 = fmaf(-d1, sc0 - 0.5f * d0, sc1);
-    sc0 = sc0 - d0;
-    sc1 = nsc1;
-    // (b) forward partials from S_j: T(la, m), T(gp, m)
-    const float t0_2 = fmaf(0.5f, d0, sc0), t0_3 = fmaf(1.f / 3.f, d0, sc0), t0_4 = fmaf(0.25f, d0, sc0);
-    const float t1_3 = fmaf(0.5f * d1, t0_3, sc1);         // T(gp, 3)
-    const float t1_4 = fmaf(d1 * (1.f / 3.f), t0_4, sc1);  // T(gp, 4)
-    // the MMA products carry the operand scales: D1 = Tbar(u, 4) / k1, D2 = Q / k2
+    const float is = in.is;
+    float trN1, tN1, tN;
+    float tp[NC][N + 1];  // forward partials T(chain_k, m) from S_j (m = k+1 .. N)
+    if constexpr (NC == 2) {
+      // depth 4 written out (the generic loops below cost ~3% at config 5)
+      const float d0 = in.dc[0], d1 = in.dc[1];
+      const float r0_3 = sc[0] - d0 * (1.f / 3.f);
+      trN1 = fmaf(-0.5f * d1, r0_3, sc[1]);  // Tr(gp, 3): the exp(-dX) partial
+      const float nsc1 = fmaf(-d1, sc[0] - 0.5f * d0, sc[1]);
+      sc[0] = sc[0] - d0;
+      sc[1] = nsc1;
+      tp[0][2] = fmaf(0.5f, d0, sc[0]);
+      tp[0][3] = fmaf(1.f / 3.f, d0, sc[0]);
+      tp[0][4] = fmaf(0.25f, d0, sc[0]);
+      tN1 = fmaf(0.5f * d1, tp[0][3], sc[1]);         // T(gp, 3)
+      tN = fmaf(d1 * (1.f / 3.f), tp[0][4], sc[1]);   // T(gp, 4)
+    } else {
+      // (a) reconstruct S_j = S_{j+1} (x) exp(-dX_j) on the chain: partials of the exp(-dX) step
+      // (targets up to N-1; Tr(gp, N-1) drives the parents' and P's reconstruction)
+      float tn[NC][N];
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        const int lv = k + 1;
+#pragma unroll
+        for (int m = lv; m < N; ++m) {
+          const float a = -in.dc[k] * (1.f / (float)(m - lv + 1));
+          tn[k][m] = (k == 0) ? sc[k] + a : fmaf(a, tn[k > 0 ? k - 1 : 0][m], sc[k]);
+        }
+      }
+      trN1 = tn[NC - 1][N - 1];  // Tr(gp, N-1)
+#pragma unroll
+      for (int k = 0; k < NC; ++k) sc[k] = tn[k][k + 1];
+      // (b) forward partials from S_j
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        const int lv = k + 1;
+#pragma unroll
+        for (int m = lv; m <= N; ++m) {
+          const float a = in.dc[k] * (1.f / (float)(m - lv + 1));
+          tp[k][m] = (k == 0) ? sc[k] + a : fmaf(a, tp[k > 0 ? k - 1 : 0][m], sc[k]);
+        }
+      }
+      tN1 = tp[NC - 1][N - 1];  // T(gp, N-1)
+      tN = tp[NC - 1][N];       // T(gp, N)
+    }
+    // the MMA products carry the operand scales: D1 = Tbar(u, N) / k1, D2 = Q / k2
     const float k1 = inv_s1 * is, k2 = inv_s2 * is;
-    const float pq = -tr3 * k2, gq = 0.5f * t1_4 * k2, gt = 0.5f * t1_4 * k1;
+    const float pq = -trN1 * k2, gq = 0.5f * tN * k2, gt = 0.5f * tN * k1;
     Sums out;
     float* v = out.v;
-    float tbp1 = 0.f, tbp2u = 0.f;  // Tbar(gp, 3), Tbar(gp, 4) / k1 from the parents
+    float tbp1 = 0.f, tbp2u = 0.f;  // Tbar(gp, N-1), Tbar(gp, N) / k1 from the parents
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      // leaf pairs: P_j = P_{j+1} - Tr(gp,3) Q_j;  gl = P_j + T(gp,4)/2 Q_j
+      // leaf pairs: P_j = P_{j+1} - Tr(gp,N-1) Q_j;  gl = P_j + T(gp,N)/2 Q_j
       const float Di = __uint_as_float(rr[4 + i]);
       P[i] = fmaf(pq, Di, P[i]);
       // parent u = gp.(4q+i): adjoint pull-back from its leaves, gradient of its letter
-      const float Du = __uint_as_float(rr[i]);  // Tbar(u, 4) / k1
-      const float lm = lm_[i];                  // Tbar(u, 3)
+      const float Du = __uint_as_float(rr[i]);  // Tbar(u, N) / k1
+      const float lm = lm_[i];                  // Tbar(u, N-1)
       tbp1 = fmaf(dy[i], lm, tbp1);
       tbp2u = fmaf(dy[i], Du, tbp2u);
-      // letter 4q+i: leaf term P_j + T(gp,4)/2 Q_j, parent term Tbar(u,3) T(gp,3) + Tbar(u,4) T(gp,4)/2
-      v[i] = fmaf(gt, Du, fmaf(lm, t1_3, fmaf(gq, Di, P[i])));
+      // letter 4q+i: leaf term P_j + T(gp,N)/2 Q_j, parent term Tbar(u,N-1) T(gp,N-1) + Tbar(u,N) T(gp,N)/2
+      v[i] = fmaf(gt, Du, fmaf(lm, tN1, fmaf(gq, Di, P[i])));
       lm_[i] = fmaf(Du, k1, lm);
     }
     const float tbp2 = 0.5f * k1 * tbp2u;
-    // chain, deepest first (trunc_backward_kernel (c) with NC = 2): node gp (level 2), then la
-    float gc1, gc0;
-    {
-      const float n2 = lc1, n3 = tbp1, n4 = tbp2;  // Tbar(gp, m), m = 2..4
-      lc1 = n2 + n3 + n4;
-      gc1 = fmaf(n2, t0_2, fmaf(0.5f * n3, t0_3, (1.f / 3.f) * n4 * t0_4));
+    // chain, deepest first (trunc_backward_kernel (c)): tbc[m] = Tbar contributed by the child
+    if constexpr (NC == 2) {
+      const float d1 = in.dc[1];
+      const float n2 = lc[1], n3 = tbp1, n4 = tbp2;  // Tbar(gp, m), m = 2..4
+      lc[1] = n2 + n3 + n4;
+      out.gc[1] = fmaf(n2, tp[0][2], fmaf(0.5f * n3, tp[0][3], (1.f / 3.f) * n4 * tp[0][4]));
       const float c2 = d1 * n2, c3 = 0.5f * d1 * n3, c4 = (1.f / 3.f) * d1 * n4;  // -> Tbar(la, m)
-      const float m1 = lc0;
-      lc0 = m1 + c2 + c3 + c4;
-      gc0 = fmaf(0.5f, c2, fmaf(1.f / 3.f, c3, fmaf(0.25f, c4, m1)));
+      const float m1 = lc[0];
+      lc[0] = m1 + c2 + c3 + c4;
+      out.gc[0] = fmaf(0.5f, c2, fmaf(1.f / 3.f, c3, fmaf(0.25f, c4, m1)));
+    } else {
+      float tbc[N + 1];
+#pragma unroll
+      for (int m = 0; m <= N; ++m) tbc[m] = 0.f;
+      tbc[N - 1] = tbp1;
+      tbc[N] = tbp2;
+#pragma unroll
+      for (int k = NC - 1; k >= 0; --k) {
+        const int lv = k + 1;
+        float tbn[N + 1];
+#pragma unroll
+        for (int m = 0; m <= N; ++m) tbn[m] = (m == lv) ? lc[k] : tbc[m];
+        float lsum = tbn[lv], gs = 0.f;
+#pragma unroll
+        for (int m = lv; m <= N; ++m) {
+          if (m > lv) lsum += tbn[m];
+          const float par = (k == 0) ? 1.f : tp[k > 0 ? k - 1 : 0][m];
+          gs = fmaf(tbn[m] * (1.f / (float)(m - lv + 1)), par, gs);
+        }
+        lc[k] = lsum;
+        out.gc[k] = gs;
+#pragma unroll
+        for (int m = 0; m <= N; ++m)
+          tbc[m] = (m >= lv) ? in.dc[k] * (1.f / (float)(m - lv + 1 > 0 ? m - lv + 1 : 1)) * tbn[m] : 0.f;
+      }
     }
-    out.gc0 = gc0;
-    out.gc1 = gc1;
     return out;
   };
 

@@ -67,26 +67,28 @@ def _autograd(X, ws, g, tc_bwd, monkeypatch):
     return Xt.grad.cpu().numpy()
 
 
+@pytest.mark.parametrize("d,N", [(16, 4), (8, 5)])
 @pytest.mark.parametrize("L", [2, 3, 17, 33, 34, 65, 200])
-def test_tc_backward_matches_oracle(L, monkeypatch):
+def test_tc_backward_matches_oracle(d, N, L, monkeypatch):
     """Chunk edges (M < 32, M = 32, M = 33, ragged last chunk) against the fp64 oracle and the
-    CUDA-core backward."""
-    ws = sk.build_truncated(16, 4)
+    CUDA-core backward, for both P/Q instantiations (config 5 and config 2 sets)."""
+    ws = sk.build_truncated(d, N)
     B = 3
-    X = brownian(40 + L, B, L, 16).astype(np.float32)
+    X = brownian(40 + L, B, L, d).astype(np.float32)
     g = np.random.default_rng(L).standard_normal((B, len(ws))).astype(np.float32)
     dX = _autograd(X, ws, g, True, monkeypatch)
-    _, dref = ora.backward(X.astype(np.float64), ws.codes, ws.lengths, 16, g.astype(np.float64))
+    _, dref = ora.backward(X.astype(np.float64), ws.codes, ws.lengths, d, g.astype(np.float64))
     assert ora.rel_err(dX, dref) <= TOL32
     assert ora.rel_err(dX, _autograd(X, ws, g, False, monkeypatch)) <= TOL32
 
 
-def test_tc_backward_scaled_inputs(monkeypatch):
+@pytest.mark.parametrize("d,N", [(16, 4), (8, 5)])
+def test_tc_backward_scaled_inputs(d, N, monkeypatch):
     """Power-of-two operand scaling: upstream rows spanning 2^-30..2^30, a path scaled by 1e4,
     one by 1e-4, a constant stretch (zero increments), a zero upstream path."""
-    ws = sk.build_truncated(16, 4)
+    ws = sk.build_truncated(d, N)
     B, L = 5, 70
-    X = brownian(77, B, L, 16)
+    X = brownian(77, B, L, d)
     X[1] *= 1e4
     X[2] *= 1e-4
     X[3, 20:40] = X[3, 20]
@@ -97,7 +99,7 @@ def test_tc_backward_scaled_inputs(monkeypatch):
     g[4] = 0.0
     g = g.astype(np.float32)
     dX = _autograd(X, ws, g, True, monkeypatch)
-    _, dref = ora.backward(X.astype(np.float64), ws.codes, ws.lengths, 16, g.astype(np.float64))
+    _, dref = ora.backward(X.astype(np.float64), ws.codes, ws.lengths, d, g.astype(np.float64))
     for b in range(B):
         assert ora.rel_err(dX[b], dref[b]) <= TOL32, b
     assert not np.any(dX[4])

@@ -15,7 +15,8 @@ import subprocess
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OBJ = os.path.join(ROOT, "paper_2602_24066_b200", "csrc", "build", "sigb_trunc.o")
 KERNELS = {
-    "trunc_pq_backward_kernel": "_ZN4sigb5trunc2pq24trunc_pq_backward_kernelEPKflllS3_llS3_llPf",
+    "trunc_pq_backward_kernel": "_ZN4sigb5trunc2pq24trunc_pq_backward_kernelILi16ELi4EEEvPKflllS4_llS4_llPf",
+    "trunc_pq_backward_kernel_d8_n5": "_ZN4sigb5trunc2pq24trunc_pq_backward_kernelILi8ELi5EEEvPKflllS4_llS4_llPf",
     "trunc_tc_forward_kernel": "_ZN4sigb5trunc2tc23trunc_tc_forward_kernelILi16ELi4EEEvPKfllPflli",
 }
 MARKERS = ("UTCHMMA", "UTCBAR", "LDTM", "STTM", "UTCATOMSWS", "SYNCS", "UBLKCP", "LDGSTS", "SHFL", "FFMA2", "FFMA")
