@@ -529,8 +529,10 @@ def run_ours(args) -> None:
         kb_name, kf_name = "sigjit_bwd", "sigjit_fwd"
     if tc_fwd:
         kf_name = "trunc_tc_forward_kernel"  # leaf level on the tensor cores (csrc/sigb_trunc_tc.cuh)
-        kb_name = {"2": "trunc_pq_backward_kernel", "1": "trunc_backward_kernel"}.get(
-            os.environ.get("SIGB_TRUNC_TC_BWD", "2"), "trunc_backward_kernel")  # csrc/sigb_trunc_pq.cuh
+    pq_bwd = (plan.kernel_kind == 1 and cfg.get("kind") == "truncated" and tdt == torch.float32
+              and (d, cfg.get("depth")) in ((16, 4), (8, 5)) and os.environ.get("SIGB_TRUNC_TC_BWD", "2") == "2")
+    if pq_bwd:
+        kb_name = "trunc_pq_backward_kernel"  # both leaf sums on the tensor cores (csrc/sigb_trunc_pq.cuh)
     roof_b = roof(kb_name, f_bwd_path, min_bwd_path, kb_ms, kb_n, bytes_bwd)
     roof_f = roof(kf_name, f_fwd_path, min_fwd_path, kf_ms, kf_n, bytes_fwd)
     dominant = roof_b if (roof_b and kb_ms >= kf_ms) else roof_f
