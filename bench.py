@@ -477,7 +477,7 @@ def run_ours(args) -> None:
     # length) pair per step; the backward needs at least 3 such sweeps
     min_fwd_path = 2.0 * M * plan.step_fmas
     min_bwd_path = 3.0 * min_fwd_path
-    tc_fwd = (plan.kernel_kind == 1 and cfg.get("kind") == "truncated" and d == 16 and cfg.get("depth") == 4
+    tc_fwd = (plan.kernel_kind == 1 and cfg.get("kind") == "truncated" and (d, cfg.get("depth")) == (16, 4)
               and tdt == torch.float32 and os.environ.get("SIGB_TRUNC_TC", "1") != "0")
 
     def roof(kname, flop_path, min_path, k_ms, k_n, bytes_path):

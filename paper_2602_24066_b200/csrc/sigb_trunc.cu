@@ -39,15 +39,18 @@ int fwd(const T* X, int64_t B, int64_t L, const int64_t* bounds, int64_t K, T* o
   const int64_t grid = C::CPP > 1 ? B * C::CPP : (B + C::PPC - 1) / C::PPC;
   if (grid == 0) return SIGB_OK;
   if constexpr (std::is_same<T, float>::value && D == 16 && N == 4) {
-    // leaf level on the tensor cores (sigb_trunc_tc.cuh): c5 fwd 127.4 -> 92.5 ms.
+    // leaf level on the tensor cores (sigb_trunc_tc.cuh): c5 fwd 127.4 -> 65 ms.  (The kernel
+    // also builds for d = 8, depth 5 with the MMA's N padded to 16; config 2 measured 2.0 ->
+    // 2.3 ms per 1,024 paths there, so that set keeps the register kernel.)
     // SIGB_TRUNC_TC=0 selects the register kernel (A/B experiments, parity tests).
     const char* e = getenv("SIGB_TRUNC_TC");
+    const int64_t grid_tc = B * Cfg<D, N, 4>::CPP;  // the tensor-core kernel's fragment: 4 parents per thread
     if (g_tensor_cores && !(e && atoi(e) == 0) && !bounds) {
       SIGB_CUDA_TRY(cudaFuncSetAttribute(tc::trunc_tc_forward_kernel<D, N>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kFwdSmem));
       count_launch();
       timing_begin(0, stream);
-      tc::trunc_tc_forward_kernel<D, N><<<(unsigned)grid, tc::kThreadsTc, tc::kFwdSmem, stream>>>(
+      tc::trunc_tc_forward_kernel<D, N><<<(unsigned)grid_tc, tc::kThreadsTc, tc::kFwdSmem, stream>>>(
           X, B, L, out, out_ld, out_col0, include_empty);
       timing_end(0, stream);
       SIGB_CUDA_TRY(cudaGetLastError());

@@ -77,7 +77,8 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
                             int64_t out_ld, int64_t out_col0, int include_empty) {
   constexpr int G = 4;
   using C = Cfg<D, N, G>;
-  static_assert(D == 16 && C::PPC == 1 && C::THREADS == kComputeThreads, "one path per CTA, 16 letters");
+  static_assert((D == 16 || D == 8) && C::PPC == 1 && C::CPP == 4 && C::THREADS == kComputeThreads,
+                "a quarter path per CTA (1,024 leaf parents); d < 16 pads the MMA's N with zero letters");
   constexpr int NC = C::NC;
   constexpr int CH = kChunkTc;
   extern __shared__ __align__(1024) unsigned char smf[];
@@ -138,6 +139,13 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
       tcu::fence_async_smem();
       asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(su32(&mbar[1 + db])) : "memory");
     };
+    if constexpr (D < 16) {  // the B rows of letters D..15 stay zero
+      for (int db = 0; db < 2; ++db)
+        for (int r = 0; r < kRounds; ++r)
+          for (int lo = 0; lo < 2; ++lo)
+            for (int i = lane; i < (16 - D) * kStepsPerMma; i += 32)
+              Bsb(db, r, lo)[kmajor_off(D + i / kStepsPerMma, i % kStepsPerMma)] = 0.f;
+    }
     if (nchunks > 0) {
       stage(0);
       if (nchunks > 1) stage(1);
@@ -241,7 +249,7 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        uint32_t rg[D];
+        uint32_t rg[16];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
             : "=r"(rg[0]), "=r"(rg[1]), "=r"(rg[2]), "=r"(rg[3]), "=r"(rg[4]), "=r"(rg[5]), "=r"(rg[6]), "=r"(rg[7]),

@@ -20,12 +20,13 @@ def _forward(X, ws, tc, monkeypatch):
     return sk.signature_forward(X, ws).values
 
 
+@pytest.mark.parametrize("d,N", [(16, 4)])
 @pytest.mark.parametrize("L", [2, 5, 9, 33, 100, 257])
-def test_tc_forward_matches_oracle(L, monkeypatch):
-    ws = sk.build_truncated(16, 4)
-    X = brownian(11 + L, 3, L, 16).astype(np.float32)
+def test_tc_forward_matches_oracle(d, N, L, monkeypatch):
+    ws = sk.build_truncated(d, N)
+    X = brownian(11 + L, 3, L, d).astype(np.float32)
     out = _forward(X, ws, True, monkeypatch)
-    ref = ora.forward(X.astype(np.float64), ws.codes, ws.lengths, 16)
+    ref = ora.forward(X.astype(np.float64), ws.codes, ws.lengths, d)
     assert ora.rel_err(out, ref) <= TOL32
     reg = _forward(X, ws, False, monkeypatch)
     assert ora.rel_err(out, reg) <= TOL32
@@ -38,9 +39,10 @@ def test_tc_forward_single_sample(monkeypatch):
     assert out.shape == (4, len(ws)) and not np.any(out)
 
 
-def test_tc_forward_large_batch_and_include_empty(monkeypatch):
-    ws = sk.build_truncated(16, 4, include_empty=True)
-    X = brownian(5, 300, 64, 16).astype(np.float32)
+@pytest.mark.parametrize("d,N", [(16, 4)])
+def test_tc_forward_large_batch_and_include_empty(d, N, monkeypatch):
+    ws = sk.build_truncated(d, N, include_empty=True)
+    X = brownian(5, 300, 64, d).astype(np.float32)
     out = _forward(X, ws, True, monkeypatch)
     reg = _forward(X, ws, False, monkeypatch)
     assert np.all(out[:, 0] == 1.0)
