@@ -261,7 +261,9 @@ extern "C" int sigb_forward(const sigb_plan* plan, int dtype, const void* d_X, i
   }
   if (use_jit(plan)) {
     rc = jit::forward(plan, dtype, d_X, B, L, d_out, out_ld, out_col0, include_empty, d_state, (cudaStream_t)stream);
-    if (rc == SIGB_OK || g_policy == 4) return rc;
+    if (rc == SIGB_OK) return rc;
+    if (g_policy == 4)
+      return rc == jit::kPending ? fail(SIGB_ERR_UNSUPPORTED, "generated kernel not ready") : rc;
     // compiling in the background (jit::kPending) or failed: the fragment kernels serve the call
     if (plan->frag.ok)
       return frag::forward(plan, dtype, d_X, B, L, nullptr, 1, d_out, out_ld, out_col0, include_empty, d_state,

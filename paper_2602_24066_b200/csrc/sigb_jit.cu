@@ -843,7 +843,7 @@ int ensure(sigb_plan* p, int dtype, bool backward, bool wait) {
   const int di = dtype == SIGB_F32 ? 0 : 1, bi = backward ? 1 : 0;
   std::lock_guard<std::mutex> lock(J.mu);
   if (J.kern[di][bi]) return SIGB_OK;
-  if (J.standin[di][bi]) return kPending;
+  if (J.standin[di][bi] && !wait) return kPending;  // a forced wait (policy 4, SIGB_JIT_SYNC) overrides the pin
   if (J.failed[di][bi]) return fail(SIGB_ERR_UNSUPPORTED, "word-set kernel compilation failed earlier");
   std::shared_ptr<Pending>& pd = J.pending[di][bi];
   if (!pd) {

@@ -46,12 +46,33 @@ def main():
         "sparse d=16 trie": sk.build_custom([(i,) for i in range(16)] + [(i, (3 * i) % 16) for i in range(16)]
                                             + [(i, (3 * i) % 16, (5 * i + 1) % 16) for i in range(0, 16, 2)], 16),
     }
-    for policy in (0, 1, 2, 3, 4):
+    for policy in (0, 1, 2, 4):
         _lib.set_kernel_policy(policy)
         for name, ws in sets.items():
             B = 70 if "sparse" in name else (2 if "16" in name else 3)  # sparse: several 32-path blocks
-            run(ws, B=B, L=24 if "16" in name else 40)
+            try:
+                run(ws, B=B, L=24 if "16" in name else 40)
+            except RuntimeError as e:  # policy 4 forces a generated kernel; report, keep going
+                print(f"policy {policy} {name}: launch refused ({e!r}): {_lib.lib().sigb_last_error()}", flush=True)
+                continue
             print(f"policy {policy} {name}: kernel kind {ws.plan().kernel_kind}", flush=True)
+    _lib.set_kernel_policy(0)
+    # round-2 paths: the tcgen05 kernels over several chunks (producer pipelines, both MMA groups),
+    # checkpoint_stride on the truncated kernels, the parallel-in-time forward
+    for d, N in ((16, 4), (8, 5)):
+        ws = sk.build_truncated(d, N)
+        run(ws, B=2, L=75)
+        X = brownian(3, 2, 75, d)
+        g = np.random.default_rng(4).standard_normal((2, ws.width))
+        sk.signature_backward(X, ws, g, checkpoint_stride=5)
+        Xt = torch.from_numpy(X.astype(np.float32)).cuda().requires_grad_(True)
+        sk.signature(Xt, ws, checkpoint_stride=7).backward(torch.from_numpy(g).float().cuda())
+        print(f"tcgen05 / checkpoint d={d} N={N}", flush=True)
+    os.environ["SIGB_SCAN"] = "2"
+    sk.signature_forward(brownian(5, 2, 300, 4), sk.build_truncated(4, 4))
+    os.environ["SIGB_SCAN"] = "1"
+    torch.cuda.synchronize()
+    print("parallel-in-time forward", flush=True)
     _lib.set_kernel_policy(0)
     print("sanitize workload done")
 
