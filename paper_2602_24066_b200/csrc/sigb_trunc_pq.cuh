@@ -160,12 +160,19 @@ __global__ void __launch_bounds__(kBlock, 1)
   float* lstage = reinterpret_cast<float*>(sm + Q_::oA2h);  // [GPC][D y][D z] fp32 (<= 64 KB = A2 hi + lo)
   float* sstage = reinterpret_cast<float*>(sm + Q_::oRed);  // [GPC][D y] parent values
   {
-    const float* lsrc = grow + Q_::off(N) + (int64_t)cip * GPC * D * D;
-    for (int i = tid; i < GPC * D * D; i += kBlock)
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tcu::su32(lstage + i)), "l"(lsrc + i) : "memory");
-    const float* ssrc = srow + Q_::off(N - 1) + (int64_t)cip * GPC * D;
-    for (int i = tid; i < GPC * D; i += kBlock)
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tcu::su32(sstage + i)), "l"(ssrc + i) : "memory");
+    // 16-byte copies when the source rows are 16-byte aligned (the usual case: no epsilon column,
+    // aligned tensors), else 4-byte ones
+    auto copy = [&](float* dst, const float* src, int n) {
+      if (((uintptr_t)src & 15) == 0) {
+        for (int i = 4 * tid; i < n; i += 4 * kBlock)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tcu::su32(dst + i)), "l"(src + i) : "memory");
+      } else {
+        for (int i = tid; i < n; i += kBlock)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tcu::su32(dst + i)), "l"(src + i) : "memory");
+      }
+    };
+    copy(lstage, grow + Q_::off(N) + (int64_t)cip * GPC * D * D, GPC * D * D);
+    copy(sstage, srow + Q_::off(N - 1) + (int64_t)cip * GPC * D, GPC * D);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
   float sc[NC], lc[NC];  // chain values S_j and (partial) adjoints; a node is seeded once (the owner)

@@ -147,3 +147,15 @@ def test_tensor_core_switch(monkeypatch):
     for S, dX in ((S_cc, d_cc), (S_tc, d_tc)):
         assert ora.rel_err(S, ref) <= TOL32
         assert ora.rel_err(dX, dref) <= TOL32
+
+
+@pytest.mark.parametrize("d,N", [(16, 4), (8, 5)])
+def test_tc_backward_epsilon_column(d, N, monkeypatch):
+    """include_empty: the upstream carries a leading epsilon column (g_col0 = 1), so the staged leaf
+    block is not 16-byte aligned and the kernel takes its 4-byte copies."""
+    ws = sk.build_truncated(d, N, include_empty=True)
+    X = brownian(95, 3, 41, d).astype(np.float32)
+    g = np.random.default_rng(96).standard_normal((3, len(ws) + 1)).astype(np.float32)
+    dX = _autograd(X, ws, g, True, monkeypatch)
+    _, dref = ora.backward(X.astype(np.float64), ws.codes, ws.lengths, d, g[:, 1:].astype(np.float64))
+    assert ora.rel_err(dX, dref) <= TOL32
