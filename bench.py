@@ -77,7 +77,8 @@ def parse_args(argv=None):
     p.add_argument("--weak", action="store_true", help="every rank runs the config's whole batch (weak scaling)")
     p.add_argument("--strong", action="store_true", help="(default) shard one fixed global batch across the ranks")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--e2e-split", type=int, default=8, help="sub-batches per e2e step (copy/compute pipeline)")
+    p.add_argument("--e2e-split", type=int, default=8,
+                   help="max sub-batches per e2e step (copy/compute pipeline; each >= 256 paths)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--gather", action="store_true", help="also time the optional NCCL all-gather of S")
     p.add_argument("--policy", type=int, default=0, help="0 auto kernels, 1 generic trie kernels only")
@@ -574,7 +575,10 @@ def run_ours(args) -> None:
         # compute.  Every sub-batch's inputs go in and its dL/dX and loss come out
         # inside the timed region; only the first H2D and the last D2H of the run
         # are exposed.
-        split = max(1, min(args.e2e_split, B))
+        # sub-batches of >= 2 ms of device work each (from this run's timed step): a sub-batch's
+        # launches and autograd bookkeeping cost ~0.1-0.3 ms, which smaller pieces cannot hide;
+        # at most --e2e-split of them
+        split = max(1, min(args.e2e_split, B // 32, int(ms_per_step / 2.0)))
         bounds_u = [(B * i // split, B * (i + 1) // split) for i in range(split)]
         ub = max(hi - lo for lo, hi in bounds_u)
         dXh = torch.empty_like(Xh).pin_memory()
