@@ -150,6 +150,44 @@ __global__ void __launch_bounds__(kBlock, 1)
     }
   }
 
+  const int nchunks = (int)((M + CH - 1) / CH);
+  auto chunk_len = [&](int c) { return (int)(M - (int64_t)c * CH < CH ? M - (int64_t)c * CH : CH); };
+  auto stage = [&](int c, int db) {  // producer: cp.async of chunk c's samples into Xs[db]
+    const int rows = chunk_len(c) + 1;
+    const float* src = X + (b * L + (int64_t)c * CH) * D;
+    float* dst = Xsb(db);
+    for (int i = lane; i < rows * D; i += 32)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tcu::su32(dst + i)), "l"(src + i) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto prepare = [&](int c, int db, bool newest_in_flight) {  // producer: Dl[db], B[db], 1/sigma[db] of chunk c
+    if (newest_in_flight) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    const int cs = chunk_len(c);
+    const float* xs = Xsb(db);
+    float* dl = Dlb(db);
+    for (int i = lane; i < cs * D; i += 32) dl[i] = xs[i + D] - xs[i];
+    __syncwarp();
+    float v[16];  // lane = step row of B; rows past the chunk are zero
+#pragma unroll
+    for (int z = 0; z < 16; ++z) v[z] = (lane < cs && z < D) ? dl[lane * D + (z % D)] : 0.f;
+    float amax = 0.f;
+#pragma unroll
+    for (int z = 0; z < 16; ++z) amax = fmaxf(amax, fabsf(v[z]));
+    const float sc = tcu::pow2_scale(amax);
+    isig(db)[lane] = 1.f / sc;
+#pragma unroll
+    for (int kg = 0; kg < 2; ++kg) {
+      float w[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] = v[8 * kg + i];
+      const int off = tcu::kmajor_off16<2>(lane, 8 * kg);
+      tcu::split8_store(w, sc, Bhi(db) + off, Blo(db) + off);
+    }
+    tcu::fence_async_smem();  // generic-proxy writes of B -> the tensor core
+    __syncwarp();
+  };
   // ---- terminal state, adjoint seeds, P, and the constant A operands ----
   // The CTA's 1,024 x D leaf adjoints (contiguous in the upstream row: the leaves of its GPC
   // grand-parents) and 1,024 parent values are staged in shared memory first (all 288 threads,
@@ -174,6 +212,10 @@ __global__ void __launch_bounds__(kBlock, 1)
     copy(lstage, grow + Q_::off(N) + (int64_t)cip * GPC * D * D, GPC * D * D);
     copy(sstage, srow + Q_::off(N - 1) + (int64_t)cip * GPC * D, GPC * D);
     asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  if (producer && nchunks > 0) {  // the first two chunks' samples load under the setup
+    stage(nchunks - 1, 0);
+    if (nchunks > 1) stage(nchunks - 2, 1);
   }
   float sc[NC], lc[NC];  // chain values S_j and (partial) adjoints; a node is seeded once (the owner)
 #pragma unroll
@@ -221,6 +263,11 @@ __global__ void __launch_bounds__(kBlock, 1)
       }
     }
   }
+  if (producer && nchunks > 0) {  // chunk 0's increments and B, prepared while the A operands are built
+    prepare(nchunks - 1, 0, false);
+    if (nchunks > 2) stage(nchunks - 3, 0);
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(tcu::su32(&mbar[2])) : "memory");
+  }
   __syncthreads();  // the staged leaf adjoints are read: their region becomes A2
   if (!producer) {
 #pragma unroll
@@ -255,44 +302,6 @@ __global__ void __launch_bounds__(kBlock, 1)
   // 1/sigma one chunk ahead (mbarrier "ready" per buffer), issues each MMA group of chunk k+1
   // as soon as the compute warps release that TMEM half in chunk k (named barriers 1, 2), and
   // runs the chunk epilogue; the compute warps never wait on a CTA-wide barrier.
-  const int nchunks = (int)((M + CH - 1) / CH);
-  auto chunk_len = [&](int c) { return (int)(M - (int64_t)c * CH < CH ? M - (int64_t)c * CH : CH); };
-  auto stage = [&](int c, int db) {  // producer: cp.async of chunk c's samples into Xs[db]
-    const int rows = chunk_len(c) + 1;
-    const float* src = X + (b * L + (int64_t)c * CH) * D;
-    float* dst = Xsb(db);
-    for (int i = lane; i < rows * D; i += 32)
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tcu::su32(dst + i)), "l"(src + i) : "memory");
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  auto prepare = [&](int c, int db, bool newest_in_flight) {  // producer: Dl[db], B[db], 1/sigma[db] of chunk c
-    if (newest_in_flight) asm volatile("cp.async.wait_group 1;" ::: "memory");
-    else asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncwarp();
-    const int cs = chunk_len(c);
-    const float* xs = Xsb(db);
-    float* dl = Dlb(db);
-    for (int i = lane; i < cs * D; i += 32) dl[i] = xs[i + D] - xs[i];
-    __syncwarp();
-    float v[16];  // lane = step row of B; rows past the chunk are zero
-#pragma unroll
-    for (int z = 0; z < 16; ++z) v[z] = (lane < cs && z < D) ? dl[lane * D + (z % D)] : 0.f;
-    float amax = 0.f;
-#pragma unroll
-    for (int z = 0; z < 16; ++z) amax = fmaxf(amax, fabsf(v[z]));
-    const float sc = tcu::pow2_scale(amax);
-    isig(db)[lane] = 1.f / sc;
-#pragma unroll
-    for (int kg = 0; kg < 2; ++kg) {
-      float w[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) w[i] = v[8 * kg + i];
-      const int off = tcu::kmajor_off16<2>(lane, 8 * kg);
-      tcu::split8_store(w, sc, Bhi(db) + off, Blo(db) + off);
-    }
-    tcu::fence_async_smem();  // generic-proxy writes of B -> the tensor core
-    __syncwarp();
-  };
   auto issue = [&](int h, int db) {  // producer: the 48 MMAs of group h (steps 16h .. 16h+15) from B[db]
     constexpr uint32_t id = tcu::idesc_f16(128, NG);
     const uint64_t bh = tcu::smem_desc(tcu::su32(Bhi(db) + h * NG * 16), 128, 256);
@@ -472,12 +481,7 @@ __global__ void __launch_bounds__(kBlock, 1)
   };
 
   if (producer) {
-    if (nchunks > 0) {
-      stage(nchunks - 1, 0);
-      if (nchunks > 1) stage(nchunks - 2, 1);
-      prepare(nchunks - 1, 0, nchunks > 1);
-      if (nchunks > 2) stage(nchunks - 3, 0);
-      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(tcu::su32(&mbar[2])) : "memory");
+    if (nchunks > 0) {  // chunk 0 was staged and prepared during the setup
       issue(1, 0);
       issue(0, 0);
     }
@@ -496,7 +500,8 @@ __global__ void __launch_bounds__(kBlock, 1)
       tcu::fence_after();
       if (k + 1 < nchunks) issue(0, db ^ 1);
       // chunk epilogue: fixed-order sum over the 8 compute warps -> partial[path part][j][z]
-      const int cs = chunk_len(c);
+      // (the last chunk's is summed by the compute warps, which have nothing else left to do)
+      const int cs = k + 1 < nchunks ? chunk_len(c) : 0;
       for (int i = lane; i < cs * D; i += 32) {
         const int s = i / D, z = i % D;
         const float a0 = red[db][0][s][z] + red[db][1][s][z], a1 = red[db][2][s][z] + red[db][3][s][z];
@@ -597,6 +602,16 @@ __global__ void __launch_bounds__(kBlock, 1)
         }
         tcu::fence_before();
         tcu::bar_arrive(h == 1 ? 1 : 2, kBlock);
+      }
+    }
+    if (nchunks > 0) {  // the last chunk's epilogue (chunk c = 0), in the same fixed order
+      tcu::bar_sync(4, kThreads);
+      const int db = (nchunks - 1) & 1, cs = chunk_len(0);
+      for (int i = tid; i < cs * D; i += kThreads) {
+        const int s = i / D, z = i % D;
+        const float a0 = red[db][0][s][z] + red[db][1][s][z], a1 = red[db][2][s][z] + red[db][3][s][z];
+        const float a2 = red[db][4][s][z] + red[db][5][s][z], a3 = red[db][6][s][z] + red[db][7][s][z];
+        partial[(((b - b0) * CPP + cip) * M + s) * D + z] = (a0 + a1) + (a2 + a3);
       }
     }
   }
