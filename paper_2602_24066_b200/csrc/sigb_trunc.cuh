@@ -542,10 +542,6 @@ struct TcBwd {
   static constexpr size_t bytes = 2 * (2 * kAHalves + 2 * kBHalves) + 4 * kSteps + 16 + 1024;  // + align slack
 };
 
-#ifndef SIGB_ABLATE  // developer ablation builds (tools/ablate.sh): drop one part of the TC backward step
-#define SIGB_ABLATE 0
-#endif
-
 // Backward.  grid: one CTA per (CTA-part of a path) -- paths [b0, b0 + nb).
 // partial layout: [(b - b0) * CPP + cip][M][D].
 template <typename T, int D, int N, int G, bool ASYNC = (D >= 16), bool TC = false, bool CK = false>
@@ -777,7 +773,7 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS, (TC || (sizeof(T) == 4 
           in.dz[4 * k] = -q4.x; in.dz[4 * k + 1] = -q4.y; in.dz[4 * k + 2] = -q4.z; in.dz[4 * k + 3] = -q4.w;
         }
       }
-      if (!(TC && SIGB_ABLATE == 6)) chen_step<T, D, N, G, false>(st, in);
+      chen_step<T, D, N, G, false>(st, in);
       if (CK) {
         // checkpoint_stride: S_{0,t_j} from the forward replay instead of the reconstruction,
         // loaded one step ahead (ck_*) so the reload does not stall the sweep.  ck_rem = j mod
@@ -824,8 +820,8 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS, (TC || (sizeof(T) == 4 
         const float kf = inv_s * inv_sig[s];
         uint32_t rr[G];
 #pragma unroll
-        for (int g = 0; g < G; ++g) rr[g] = SIGB_ABLATE == 5 ? 0u : tcu::tmem_ld1(tmem + lane_addr + TcBwd::kSteps * (mt0 + g) + s);
-        if (SIGB_ABLATE != 5) tcu::tmem_ld_wait();
+        for (int g = 0; g < G; ++g) rr[g] = tcu::tmem_ld1(tmem + lane_addr + TcBwd::kSteps * (mt0 + g) + s);
+        tcu::tmem_ld_wait();
 #pragma unroll
         for (int g = 0; g < G; ++g) tbv[g] = __uint_as_float(rr[g]) * kf;
       }
@@ -836,7 +832,7 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS, (TC || (sizeof(T) == 4 
         if constexpr (TC) {
           const float2 tm2 = make_float2(tm, tm);
 #pragma unroll
-          for (int z = 0; z < (SIGB_ABLATE == 2 ? 0 : D); z += 2) {
+          for (int z = 0; z < D; z += 2) {
             const float2 r = __ffma2_rn(make_float2(lam.leaf[g][z], lam.leaf[g][z + 1]), tm2,
                                         make_float2(gl[z], gl[z + 1]));
             gl[z] = r.x;
@@ -898,7 +894,7 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS, (TC || (sizeof(T) == 4 
         tbc[N - 1] = tbp1;
         tbc[N] = tbp2;
 #pragma unroll
-        for (int k = NC - 1; k >= (TC && SIGB_ABLATE == 3 ? NC : 0); --k) {
+        for (int k = NC - 1; k >= 0; --k) {
           const int lv = k + 1;
           T tbn[N + 1];
 #pragma unroll
@@ -920,8 +916,7 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS, (TC || (sizeof(T) == 4 
       }
       // (d) reduce within the path's lanes; park per-warp results in shared memory
       int idx;
-      if (TC && SIGB_ABLATE == 1) idx = lane & 15;
-      else if constexpr (PERM) idx = transpose_reduce_perm<T, D>(gl, lane);
+      if constexpr (PERM) idx = transpose_reduce_perm<T, D>(gl, lane);
       else idx = transpose_reduce<T, D, C::RW>(gl, lane);
       constexpr int plain_bits = C::RW / (D < C::RW ? D : C::RW);  // lanes sharing one letter
       // one writer per letter: the plain (duplicating) stages are lane bits 2 (and 1 for
