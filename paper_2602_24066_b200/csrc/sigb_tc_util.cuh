@@ -47,6 +47,19 @@ __device__ __forceinline__ void mma_ss_f16(uint32_t d, uint64_t adesc, uint64_t 
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
 }
 
+// the same, issued by the calling thread alone (inside a one-lane branch: no elect, no
+// warp-collective sequence around each MMA)
+__device__ __forceinline__ void mma_ss_f16_1t(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit_1t(uint64_t* mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(mbar))
+               : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* mbar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"

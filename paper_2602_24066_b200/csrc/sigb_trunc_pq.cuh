@@ -117,7 +117,9 @@ __global__ void __launch_bounds__(kBlock, 1)
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + Q_::oBar);
   uint32_t* slot = reinterpret_cast<uint32_t*>(sm + Q_::oSlot);
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // warp index through a shuffle: provably warp-uniform, so the producer branch is uniform and the
+  // MMA issue inside it compiles to plain uniform-datapath UTCHMMAs (no per-MMA collective sequence)
+  const int tid = threadIdx.x, lane = tid & 31, warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const bool producer = warp == kThreads / 32;
   const int64_t b = b0 + blockIdx.x / CPP;  // the grid covers live paths only
   const int cip = blockIdx.x % CPP;
@@ -165,13 +167,19 @@ __global__ void __launch_bounds__(kBlock, 1)
     else asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncwarp();
     const int cs = chunk_len(c);
-    const float* xs = Xsb(db);
-    float* dl = Dlb(db);
-    for (int i = lane; i < cs * D; i += 32) dl[i] = xs[i + D] - xs[i];
+    const float4* xs = reinterpret_cast<const float4*>(Xsb(db));
+    float4* dl = reinterpret_cast<float4*>(Dlb(db));
+    for (int i = lane; i < cs * D / 4; i += 32) {
+      const float4 a = xs[i], n = xs[i + D / 4];
+      dl[i] = make_float4(n.x - a.x, n.y - a.y, n.z - a.z, n.w - a.w);
+    }
     __syncwarp();
     float v[16];  // lane = step row of B; rows past the chunk are zero
 #pragma unroll
-    for (int z = 0; z < 16; ++z) v[z] = (lane < cs && z < D) ? dl[lane * D + (z % D)] : 0.f;
+    for (int z4 = 0; z4 < 4; ++z4) {
+      const float4 t = (lane < cs && 4 * z4 < D) ? dl[lane * (D / 4) + z4 % (D / 4)] : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[4 * z4] = t.x; v[4 * z4 + 1] = t.y; v[4 * z4 + 2] = t.z; v[4 * z4 + 3] = t.w;
+    }
     float amax = 0.f;
 #pragma unroll
     for (int z = 0; z < 16; ++z) amax = fmaxf(amax, fabsf(v[z]));
@@ -286,7 +294,10 @@ __global__ void __launch_bounds__(kBlock, 1)
   tcu::fence_before();
   __syncthreads();
   tcu::fence_after();
-  const uint32_t tmem = *slot;
+  // the CTA owns all 512 columns, so the allocator can only return lane 0 / column 0: the TMEM
+  // addresses below are compile-time constants (uniform-datapath MMA issue, no per-MMA R2UR)
+  if (*slot != 0u) __trap();
+  constexpr uint32_t tmem = 0u;
   // chain letters' home lanes: mk[k][i] selects slot i (letter 4q+i) of the lane whose quad holds cl[k]
   float mk[NC][4];
 #pragma unroll
@@ -480,6 +491,19 @@ __global__ void __launch_bounds__(kBlock, 1)
     return out;
   };
 
+  // chunk epilogue: fixed-order sum over the 8 compute warps' parked letter sums of chunk c (buffer
+  // db) -> partial[path part][step][letter], four letters per float4
+  auto sum_parked = [&](int db, int cs, int c, int t0, int nt) {
+    float4* dst = reinterpret_cast<float4*>(partial + (((b - b0) * CPP + cip) * M + (int64_t)c * CH) * D);
+    for (int i = t0; i < cs * D / 4; i += nt) {
+      float4 w[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) w[k] = reinterpret_cast<const float4*>(&red[db][k][0][0])[i];
+      auto add = [](float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); };
+      dst[i] = add(add(add(w[0], w[1]), add(w[2], w[3])), add(add(w[4], w[5]), add(w[6], w[7])));
+    }
+  };
+
   if (producer) {
     if (nchunks > 0) {  // chunk 0 was staged and prepared during the setup
       issue(1, 0);
@@ -499,15 +523,9 @@ __global__ void __launch_bounds__(kBlock, 1)
       tcu::bar_sync(2, kBlock);  // chunk k's group 0 is read and red[db] is complete
       tcu::fence_after();
       if (k + 1 < nchunks) issue(0, db ^ 1);
-      // chunk epilogue: fixed-order sum over the 8 compute warps -> partial[path part][j][z]
-      // (the last chunk's is summed by the compute warps, which have nothing else left to do)
-      const int cs = k + 1 < nchunks ? chunk_len(c) : 0;
-      for (int i = lane; i < cs * D; i += 32) {
-        const int s = i / D, z = i % D;
-        const float a0 = red[db][0][s][z] + red[db][1][s][z], a1 = red[db][2][s][z] + red[db][3][s][z];
-        const float a2 = red[db][4][s][z] + red[db][5][s][z], a3 = red[db][6][s][z] + red[db][7][s][z];
-        partial[(((b - b0) * CPP + cip) * M + (int64_t)c * CH + s) * D + z] = (a0 + a1) + (a2 + a3);
-      }
+      // chunk epilogue (the last chunk's is summed by the compute warps, which have nothing else
+      // left to do)
+      if (k + 1 < nchunks) sum_parked(db, chunk_len(c), c, lane, 32);
     }
   } else {
     for (int k = 0; k < nchunks; ++k) {
@@ -606,13 +624,7 @@ __global__ void __launch_bounds__(kBlock, 1)
     }
     if (nchunks > 0) {  // the last chunk's epilogue (chunk c = 0), in the same fixed order
       tcu::bar_sync(4, kThreads);
-      const int db = (nchunks - 1) & 1, cs = chunk_len(0);
-      for (int i = tid; i < cs * D; i += kThreads) {
-        const int s = i / D, z = i % D;
-        const float a0 = red[db][0][s][z] + red[db][1][s][z], a1 = red[db][2][s][z] + red[db][3][s][z];
-        const float a2 = red[db][4][s][z] + red[db][5][s][z], a3 = red[db][6][s][z] + red[db][7][s][z];
-        partial[(((b - b0) * CPP + cip) * M + s) * D + z] = (a0 + a1) + (a2 + a3);
-      }
+      sum_parked((nchunks - 1) & 1, chunk_len(0), 0, tid, kThreads);
     }
   }
   tcu::fence_before();

@@ -91,7 +91,9 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
   uint32_t* slot = reinterpret_cast<uint32_t*>(smf + fSlot);
   float* stage_out = reinterpret_cast<float*>(smf + fOut);
 
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // warp index through a shuffle: provably warp-uniform, so the role branches are uniform and the
+  // MMA issue compiles to plain uniform-datapath UTCHMMAs
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
   const bool producer = warp == kComputeThreads / 32;      // issues the MMAs
   const bool stager = warp == kComputeThreads / 32 + 1;    // samples, increments, B operands
   const int64_t M = L - 1;
