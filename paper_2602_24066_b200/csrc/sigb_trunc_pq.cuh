@@ -80,7 +80,11 @@ struct PQ {
   static constexpr int oDl = oXs + 2 * 4 * (CH + 1) * D; // [2][CH][D] increments
   static constexpr int oRed = oDl + 2 * 4 * CH * D;      // [2][8 warps][CH][D] per-warp letter sums
   static constexpr int oSig = oRed + 2 * 4 * 8 * CH * D; // [2][CH] 1 / sigma per step
-  static constexpr int oBar = oSig + 2 * 4 * CH;         // mbarriers: MMA group 0, 1; increments ready 0, 1
+  // depth 4 (NC == 2): per warp and step, the grand-parents' parent-adjoint sums and chain inputs
+  // for the deferred chain sweep, [8 warps][CH][8 grand-parents][T1, T2, d1, S (even gp) / d0 (odd)]
+  static constexpr bool kDeferChain = NC == 2;
+  static constexpr int oPark = oSig + 2 * 4 * CH;
+  static constexpr int oBar = oPark + (kDeferChain ? 8 * CH * 32 * 4 : 0);  // mbarriers: MMA groups 0, 1; ready 0, 1
   static constexpr int oSlot = oBar + 32;
   static constexpr size_t kSmem = oSlot + 16;
 };
@@ -114,6 +118,7 @@ __global__ void __launch_bounds__(kBlock, 1)
   auto Dlb = [&](int db) { return reinterpret_cast<float*>(sm + Q_::oDl) + db * CH * D; };
   float(*red)[8][CH][D] = reinterpret_cast<float(*)[8][CH][D]>(sm + Q_::oRed);
   auto isig = [&](int db) { return reinterpret_cast<float*>(sm + Q_::oSig) + db * CH; };
+  float* park = reinterpret_cast<float*>(sm + Q_::oPark);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + Q_::oBar);
   uint32_t* slot = reinterpret_cast<uint32_t*>(sm + Q_::oSlot);
 
@@ -232,6 +237,14 @@ __global__ void __launch_bounds__(kBlock, 1)
     const bool owner = q == 0 && gp % trunc::ipow(D, NC - 1 - k) == 0;
     lc[k] = owner ? grow[chain_index(k)] : 0.f;
   }
+  // deferred chain (depth 4): the swept grand-parent (gp & ~7) + (lane & 7)'s adjoints -- level 2
+  // (its own node) and its share of level 1 (seeded by the first grand-parent under that letter)
+  float sw1 = 0.f, sw0 = 0.f;
+  if constexpr (Q_::kDeferChain) {
+    const int gps = (gp & ~7) + (lane & 7);
+    sw1 = grow[Q_::off(2) + gps];
+    sw0 = gps % D == 0 ? grow[Q_::off(1) + gps / D] : 0.f;
+  }
   float lm_[4], P[4] = {0.f, 0.f, 0.f, 0.f};  // (the P/Q form never reads the parents' S_j)
 #pragma unroll
   for (int g = 0; g < 4; ++g) lm_[g] = grow[par_index(4 * q + g)];
@@ -299,6 +312,7 @@ __global__ void __launch_bounds__(kBlock, 1)
   if (*slot != 0u) __trap();
   constexpr uint32_t tmem = 0u;
   // chain letters' home lanes: mk[k][i] selects slot i (letter 4q+i) of the lane whose quad holds cl[k]
+  // (the in-loop chain of depth > 4 only)
   float mk[NC][4];
 #pragma unroll
   for (int k = 0; k < NC; ++k)
@@ -354,19 +368,31 @@ __global__ void __launch_bounds__(kBlock, 1)
   // a step's letter sums before the cross-lane reduction: the reduction of step s is issued after
   // the arithmetic of step s-1 (source order), so its shuffle latency overlaps that arithmetic
   struct Sums {
-    float v[4], gc[NC];
+    float v[4], gc[NC];  // depth 4: gc[0], gc[1] = this lane's parent-adjoint sums T1, T2 (see park)
+    float x;             // depth 4: the lane's chain input for the park (d1, S_j(level 1) or d0)
   };
+  float* park_w = park + warp * CH * 32;
   auto reduce = [&](Sums& u, int s, float(*redw)[D]) {
     float* v = u.v;
-    // the quad group's partial chain terms -> full per grand-parent, added at the lane of their letter
+    if constexpr (Q_::kDeferChain) {
+      // park the grand-parent's T1 = Tbar(gp, 3), T2 = Tbar(gp, 4) contributions (summed over the quad:
+      // transposing over lane bit 0, then plain over bit 1) and S_j(level 1) for the deferred sweep
+      const bool b0 = (lane & 1) != 0;
+      float keep = b0 ? u.gc[1] : u.gc[0];
+      keep += __shfl_xor_sync(0xffffffffu, b0 ? u.gc[0] : u.gc[1], 1);
+      keep += __shfl_xor_sync(0xffffffffu, keep, 2);
+      park_w[s * 32 + lane] = (lane & 2) ? u.x : keep;
+    } else {
+      // the quad group's partial chain terms -> full per grand-parent, added at the lane of their letter
 #pragma unroll
-    for (int msk = 1; msk < QPG; msk *= 2)
+      for (int msk = 1; msk < QPG; msk *= 2)
 #pragma unroll
-      for (int k = 0; k < NC; ++k) u.gc[k] += __shfl_xor_sync(0xffffffffu, u.gc[k], msk);
+        for (int k = 0; k < NC; ++k) u.gc[k] += __shfl_xor_sync(0xffffffffu, u.gc[k], msk);
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int k = 0; k < NC; ++k) v[i] = fmaf(mk[k][i], u.gc[k], v[i]);
+        for (int k = 0; k < NC; ++k) v[i] = fmaf(mk[k][i], u.gc[k], v[i]);
+    }
     // sum over the warp's grand-parents: transposing over lane bits 4 and 3 (one letter per lane
     // group), plain over the grand-parent bits below
     const bool u4 = (lane & 16) != 0, u3 = (lane & 8) != 0;
@@ -453,15 +479,14 @@ __global__ void __launch_bounds__(kBlock, 1)
     }
     const float tbp2 = 0.5f * k1 * tbp2u;
     // chain, deepest first (trunc_backward_kernel (c)): tbc[m] = Tbar contributed by the child
-    if constexpr (NC == 2) {
-      const float d1 = in.dc[1];
-      const float n2 = lc[1], n3 = tbp1, n4 = tbp2;  // Tbar(gp, m), m = 2..4
-      lc[1] = n2 + n3 + n4;
-      out.gc[1] = fmaf(n2, tp[0][2], fmaf(0.5f * n3, tp[0][3], (1.f / 3.f) * n4 * tp[0][4]));
-      const float c2 = d1 * n2, c3 = 0.5f * d1 * n3, c4 = (1.f / 3.f) * d1 * n4;  // -> Tbar(la, m)
-      const float m1 = lc[0];
-      lc[0] = m1 + c2 + c3 + c4;
-      out.gc[0] = fmaf(0.5f, c2, fmaf(1.f / 3.f, c3, fmaf(0.25f, c4, m1)));
+    if constexpr (Q_::kDeferChain) {
+      // the chain's reverse is a pure sink (its adjoints feed only the chain letters' gradients):
+      // swept once per grand-parent after the chunk (chain_sweep), from the parked T1, T2, S_j
+      out.gc[0] = tbp1;
+      out.gc[1] = tbp2;
+      // quad lane 2 parks d1 (its grand-parent's letter), lane 3 the warp-common S_j(la) (even
+      // grand-parents) or d0 (odd ones)
+      out.x = (lane & 1) ? ((lane & 4) ? in.dc[0] : sc[0]) : in.dc[1];
     } else {
       float tbc[N + 1];
 #pragma unroll
@@ -501,6 +526,83 @@ __global__ void __launch_bounds__(kBlock, 1)
       for (int k = 0; k < 8; ++k) w[k] = reinterpret_cast<const float4*>(&red[db][k][0][0])[i];
       auto add = [](float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); };
       dst[i] = add(add(add(w[0], w[1]), add(w[2], w[3])), add(add(w[4], w[5]), add(w[6], w[7])));
+    }
+  };
+
+  // Deferred chain sweep of one chunk (depth 4), per compute warp after its steps: lane (g, quarter
+  // qq) walks grand-parent g's chain over steps 8qq+7 .. 8qq (high to low, as the reverse sweep),
+  // the carried adjoints entering each quarter through a suffix scan over the quad:
+  //   Tbar(gp,2): n2 <- n2 + T1 + T2,  gl[cl1] += n2 T(la,2) + T1/2 T(la,3) + T2/3 T(la,4)
+  //   Tbar(la,1): m1 <- m1 + c2 + c3 + c4 (c = d1 n2, d1 T1/2, d1 T2/3),
+  //               gl[cl0] += m1 + c2/2 + c3/3 + c4/4           (trunc_backward_kernel (c), depth 4)
+  // with T(la, m) = S_j(la) + d0/m.  The chain letters' sums are added to the warp's parked letter
+  // sums (cl1 per grand-parent; cl0 is common to the warp's 8 grand-parents: summed over them first).
+  auto chain_sweep = [&](int db, int cs, float(*redw)[D]) {
+    if constexpr (Q_::kDeferChain) {
+      __syncwarp();  // the parked values and the steps' letter sums of this warp
+      // lane = (grand-parent g = lane & 7, quarter qq = lane >> 3): a quarter's 8 grand-parents read
+      // one 128-byte park row per step (conflict-free)
+      const int g = lane & 7, qq = lane >> 3;
+      const int gps = (gp & ~7) + g;  // the swept grand-parent
+      const int c0 = gps / D, c1 = gps % D;
+      float t1[8], t2[8], s0[8], d0[8], d1[8];
+      float A = 0.f;
+#pragma unroll
+      for (int i = 7; i >= 0; --i) {
+        const int st = 8 * qq + i;
+        float4 pk = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (st < cs) pk = *reinterpret_cast<const float4*>(park_w + st * 32 + 4 * g);
+        const float other = __shfl_xor_sync(0xffffffffu, pk.w, 1);
+        t1[i] = pk.x; t2[i] = pk.y; d1[i] = pk.z;
+        s0[i] = (g & 1) ? other : pk.w;
+        d0[i] = (g & 1) ? pk.w : other;
+        A += t1[i] + t2[i];
+      }
+      // suffix scan over the quarters (quarter 3 is swept first): carry-in and chunk total
+      auto scan = [&](float x, float& carry_in, float& total) {
+        float inc = x;
+        float o = __shfl_down_sync(0xffffffffu, inc, 8);
+        if (qq < 3) inc += o;
+        o = __shfl_down_sync(0xffffffffu, inc, 16);
+        if (qq < 2) inc += o;
+        o = __shfl_down_sync(0xffffffffu, inc, 8);
+        carry_in = qq < 3 ? o : 0.f;
+        total = __shfl_sync(0xffffffffu, inc, g);
+      };
+      float in1, tot1;
+      scan(A, in1, tot1);
+      float n2 = sw1 + in1, C = 0.f;
+      float cg[8], csum[8];
+#pragma unroll
+      for (int i = 7; i >= 0; --i) {
+        const float tp2 = fmaf(0.5f, d0[i], s0[i]), tp3 = fmaf(1.f / 3.f, d0[i], s0[i]);
+        const float tp4 = fmaf(0.25f, d0[i], s0[i]);
+        const float n3 = t1[i], n4 = t2[i];
+        const float gc1 = fmaf(n2, tp2, fmaf(0.5f * n3, tp3, (1.f / 3.f) * n4 * tp4));
+        const float c2 = d1[i] * n2, c3 = 0.5f * d1[i] * n3, c4 = (1.f / 3.f) * d1[i] * n4;
+        n2 = n2 + n3 + n4;
+        cg[i] = fmaf(0.5f, c2, fmaf(1.f / 3.f, c3, 0.25f * c4));
+        csum[i] = c2 + c3 + c4;
+        C += csum[i];
+        const int st = 8 * qq + i;
+        if (st < cs) redw[st][c1] += gc1;
+      }
+      float in2, tot2;
+      scan(C, in2, tot2);
+      __syncwarp();  // the cl1 additions above may target a cl0 entry added below
+      float m1 = sw0 + in2;
+#pragma unroll
+      for (int i = 7; i >= 0; --i) {
+        float t = m1 + cg[i];
+        m1 += csum[i];
+        t += __shfl_xor_sync(0xffffffffu, t, 1);
+        t += __shfl_xor_sync(0xffffffffu, t, 2);
+        t += __shfl_xor_sync(0xffffffffu, t, 4);
+        const int st = 8 * qq + i;
+        if (g == 0 && st < cs) redw[st][c0] += t;
+      }
+      sw1 += tot1;
+      sw0 += tot2;
     }
   };
 
@@ -618,6 +720,7 @@ __global__ void __launch_bounds__(kBlock, 1)
           }
           reduce(pend, s + 1, redw);
         }
+        if (h == 0) chain_sweep(db, cs, redw);  // before red[db] is released to the epilogue
         tcu::fence_before();
         tcu::bar_arrive(h == 1 ? 1 : 2, kBlock);
       }
