@@ -210,20 +210,36 @@ __global__ void __launch_bounds__(kBlock, 1)
   const float* grow = gup + b * g_ld + g_col0;
   float* lstage = reinterpret_cast<float*>(sm + Q_::oA2h);  // [GPC][D y][D z] fp32 (<= 64 KB = A2 hi + lo)
   float* sstage = reinterpret_cast<float*>(sm + Q_::oRed);  // [GPC][D y] parent values
+  // Staged positions.  At d = 16 the 16-byte chunks are XOR-swizzled so that every read below is
+  // bank-conflict free: row y of grand-parent gl sits in bank half (y ^ gl) & 1 and its chunk z/4
+  // at slot (z/4) ^ (y/4) (the P terms read chunk q of one row across a warp's 8 grand-parents x 4
+  // quads, the A1 rows read chunk j of rows 4q+g); a grand-parent's parent values are spread over
+  // the banks by (gl/2) & 3.  Chunks stay whole, so 16-byte copies still apply.
+  auto lidx = [](int gl, int y, int z) {
+    if constexpr (D == 16) return gl * 256 + ((y ^ (gl & 1)) << 4) + ((((z >> 2) ^ (y >> 2)) & 3) << 2) + (z & 3);
+    else return (gl * D + y) * D + z;
+  };
+  auto sidx = [](int gl, int y) {
+    if constexpr (D == 16) return gl * 16 + (y ^ (((gl >> 1) & 3) << 2));
+    else return gl * D + y;
+  };
   {
-    // 16-byte copies when the source rows are 16-byte aligned (the usual case: no epsilon column,
-    // aligned tensors), else 4-byte ones
-    auto copy = [&](float* dst, const float* src, int n) {
+    // 16-byte copies when the source rows are 16-byte aligned (no epsilon column, aligned tensors;
+    // config 5's leaf block starts at word 4,369, so usually not), else 4-byte ones
+    auto copy = [&](float* dst, const float* src, int n, auto pos) {
       if (((uintptr_t)src & 15) == 0) {
         for (int i = 4 * tid; i < n; i += 4 * kBlock)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tcu::su32(dst + i)), "l"(src + i) : "memory");
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tcu::su32(dst + pos(i))), "l"(src + i)
+                       : "memory");
       } else {
         for (int i = tid; i < n; i += kBlock)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tcu::su32(dst + i)), "l"(src + i) : "memory");
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tcu::su32(dst + pos(i))), "l"(src + i)
+                       : "memory");
       }
     };
-    copy(lstage, grow + Q_::off(N) + (int64_t)cip * GPC * D * D, GPC * D * D);
-    copy(sstage, srow + Q_::off(N - 1) + (int64_t)cip * GPC * D, GPC * D);
+    copy(lstage, grow + Q_::off(N) + (int64_t)cip * GPC * D * D, GPC * D * D,
+         [&](int i) { return lidx(i / (D * D), (i / D) % D, i % D); });
+    copy(sstage, srow + Q_::off(N - 1) + (int64_t)cip * GPC * D, GPC * D, [&](int i) { return sidx(i / D, i % D); });
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
   if (producer && nchunks > 0) {  // the first two chunks' samples load under the setup
@@ -251,13 +267,14 @@ __global__ void __launch_bounds__(kBlock, 1)
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   const int gl_ = (gp - GPC * cip) & (GPC - 1);  // grand-parent within the CTA (valid for the producer too)
-  const float* lg = lstage + gl_ * D * D;
+  // Lambda[gl_, y, 4j .. 4j+3] as a float4
+  auto lchunk = [&](int y, int j) { return *reinterpret_cast<const float4*>(lstage + lidx(gl_, y, 4 * j)); };
   float a2v[4][D];  // Lambda[gp, y, 4q + i]: this thread's A2 rows (held across the barrier below)
   float amax1 = 0.f, amax2 = 0.f;
 #pragma unroll
   for (int y = 0; y < D; ++y) {
-    const float sy = sstage[gl_ * D + y];
-    const float4 l4 = *reinterpret_cast<const float4*>(lg + y * D + 4 * q);
+    const float sy = sstage[sidx(gl_, y)];
+    const float4 l4 = lchunk(y, q);
     a2v[0][y] = l4.x; a2v[1][y] = l4.y; a2v[2][y] = l4.z; a2v[3][y] = l4.w;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -268,7 +285,10 @@ __global__ void __launch_bounds__(kBlock, 1)
 #pragma unroll
   for (int g = 0; g < 4; ++g)
 #pragma unroll
-    for (int z = 0; z < D; ++z) amax1 = fmaxf(amax1, fabsf(lg[(4 * q + g) * D + z]));
+    for (int j = 0; j < D / 4; ++j) {
+      const float4 t = lchunk(4 * q + g, j);
+      amax1 = fmaxf(fmaxf(amax1, fmaxf(fabsf(t.x), fabsf(t.y))), fmaxf(fabsf(t.z), fabsf(t.w)));
+    }
   const float s1 = tcu::pow2_scale(amax1), s2 = tcu::pow2_scale(amax2);
   const float inv_s1 = 1.f / s1, inv_s2 = 1.f / s2;  // exact: powers of two
   if (!producer) {
@@ -278,7 +298,10 @@ __global__ void __launch_bounds__(kBlock, 1)
       for (int kg = 0; kg < 2; ++kg) {
         float v[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = 8 * kg + i < D ? lg[(4 * q + g) * D + 8 * kg + i] : 0.f;
+        for (int h = 0; h < 2; ++h) {
+          const float4 t = 8 * kg + 4 * h < D ? lchunk(4 * q + g, 2 * kg + h) : make_float4(0.f, 0.f, 0.f, 0.f);
+          v[4 * h] = t.x; v[4 * h + 1] = t.y; v[4 * h + 2] = t.z; v[4 * h + 3] = t.w;
+        }
         const int off = (mt0 + g) * kRowHalves + tcu::kmajor_off16<2>(r, 8 * kg);
         tcu::split8_store(v, s1, A1h + off, A1l + off);
       }
