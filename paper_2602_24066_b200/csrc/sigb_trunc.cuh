@@ -32,7 +32,13 @@ namespace trunc {
 constexpr int kChunkT = 32;  // backward steps staged per chunk (16 where the reduction buffers would not fit)
 constexpr int kThreadsT = 256;
 
-__host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
+// iterative (not recursive): with an unrolled loop index as exponent it inlines and folds to a
+// constant instead of compiling to a device-function call, whose CALL waits on every load in flight
+__host__ __device__ constexpr int ipow(int b, int e) {
+  int r = 1;
+  for (int i = 0; i < e; ++i) r *= b;
+  return r;
+}
 
 template <int D, int N, int G>
 struct Cfg {
@@ -51,7 +57,11 @@ struct Cfg {
   static_assert(D <= (TPP < 32 ? TPP : 32), "letters must not exceed the reduction width");
   static_assert(TPP < kThreadsT ? kThreadsT % TPP == 0 : TPP % kThreadsT == 0, "CTA tiling");
   // level offsets in canonical order: O[l] = sum_{k=1}^{l-1} D^k
-  __host__ __device__ static constexpr int64_t off(int l) { return l <= 1 ? 0 : off(l - 1) + ipow(D, l - 1); }
+  __host__ __device__ static constexpr int64_t off(int l) {
+    int64_t o = 0;
+    for (int k = 1; k < l; ++k) o += ipow(D, k);
+    return o;
+  }
 };
 
 template <typename T, int R>
