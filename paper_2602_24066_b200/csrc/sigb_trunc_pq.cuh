@@ -614,16 +614,23 @@ __global__ void __launch_bounds__(kBlock, 1)
       scan(C, in2, tot2);
       __syncwarp();  // the cl1 additions above may target a cl0 entry added below
       float m1 = sw0 + in2;
+      float t[8];
 #pragma unroll
       for (int i = 7; i >= 0; --i) {
-        float t = m1 + cg[i];
+        t[i] = m1 + cg[i];
         m1 += csum[i];
-        t += __shfl_xor_sync(0xffffffffu, t, 1);
-        t += __shfl_xor_sync(0xffffffffu, t, 2);
-        t += __shfl_xor_sync(0xffffffffu, t, 4);
-        const int st = 8 * qq + i;
-        if (g == 0 && st < cs) redw[st][c0] += t;
       }
+      // sum over the 8 grand-parents transposing over lane bits 2, 1, 0: lane g ends with step 8qq+g
+      float u[4], w[2];
+      const bool b2 = (g & 4) != 0, b1 = (g & 2) != 0, b0 = (g & 1) != 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        u[k] = (b2 ? t[4 + k] : t[k]) + __shfl_xor_sync(0xffffffffu, b2 ? t[k] : t[4 + k], 4);
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        w[k] = (b1 ? u[2 + k] : u[k]) + __shfl_xor_sync(0xffffffffu, b1 ? u[k] : u[2 + k], 2);
+      const float tg = (b0 ? w[1] : w[0]) + __shfl_xor_sync(0xffffffffu, b0 ? w[0] : w[1], 1);
+      if (8 * qq + g < cs) redw[8 * qq + g][c0] += tg;
       sw1 += tot1;
       sw0 += tot2;
     }
