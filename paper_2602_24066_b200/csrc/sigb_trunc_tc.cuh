@@ -246,6 +246,13 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
     // written with consecutive threads on consecutive words (the CTA's leaves are one contiguous
     // block of 16,384 words; its parents one block of 1,024)
     const int pl0 = (f.gp - (int)(f.cip * (kComputeThreads / C::Q))) * D + f.q * G;  // first parent in the CTA
+    // staged position of (parent row, letter z): at d = 16 the 16-byte chunk is XOR-swizzled by row/4 and
+    // odd row quads of 16 swap row parity, so the eight 16-byte stores of a phase (rows 4 apart) and
+    // the linear read-back both hit distinct banks
+    auto spos = [](int row, int z) {
+      if constexpr (D == 16) return ((row ^ ((row >> 4) & 1)) << 4) + ((((z >> 2) ^ (row >> 2)) & 3) << 2) + (z & 3);
+      else return row * D + z;
+    };
     if (nch > 0) {
       mbar_wait(&mbar[0], (uint32_t)((nch - 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;");
@@ -259,23 +266,23 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
               "=r"(rg[15])
             : "r"(tmem + lane_addr + 16 * (mt0 + g)));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        float4* dst = reinterpret_cast<float4*>(stage_out + (pl0 + g) * D);
 #pragma unroll
         for (int z = 0; z < D; z += 4)
-          dst[z / 4] = make_float4(__uint_as_float(rg[z]), __uint_as_float(rg[z + 1]), __uint_as_float(rg[z + 2]),
-                                   __uint_as_float(rg[z + 3]));
+          *reinterpret_cast<float4*>(stage_out + spos(pl0 + g, z)) =
+              make_float4(__uint_as_float(rg[z]), __uint_as_float(rg[z + 1]), __uint_as_float(rg[z + 2]),
+                          __uint_as_float(rg[z + 3]));
       }
     } else {
 #pragma unroll
       for (int g = 0; g < G; ++g)
 #pragma unroll
-        for (int z = 0; z < D; ++z) stage_out[(pl0 + g) * D + z] = 0.f;
+        for (int z = 0; z < D; ++z) stage_out[spos(pl0 + g, z)] = 0.f;
     }
     bar_sync(2, kComputeThreads);  // the CTA's leaf block is staged
     if (f.b < B) {
       float* orow = out + f.b * out_ld + out_col0;
       float* leaves = orow + C::off(N) + (int64_t)f.cip * (kComputeThreads / C::Q) * D * D;
-      for (int i = tid; i < (kComputeThreads / C::Q) * D * D; i += kComputeThreads) leaves[i] = stage_out[i];
+      for (int i = tid; i < (kComputeThreads / C::Q) * D * D; i += kComputeThreads) leaves[i] = stage_out[spos(i / D, i % D)];
 #pragma unroll
       for (int k = 0; k < NC; ++k)
         if (f.chain_owner(k)) orow[f.chain_index(k)] = ch[k];
