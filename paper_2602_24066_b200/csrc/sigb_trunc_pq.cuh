@@ -84,7 +84,10 @@ struct PQ {
   // for the deferred chain sweep, [8 warps][CH][8 grand-parents][T1, T2, d1, S (even gp) / d0 (odd)]
   static constexpr bool kDeferChain = NC == 2;
   static constexpr int oPark = oSig + 2 * 4 * CH;
-  static constexpr int oBar = oPark + (kDeferChain ? 8 * CH * 32 * 4 : 0);  // mbarriers: MMA groups 0, 1; ready 0, 1
+  // depth 4: per warp, the chain values of its 8 grand-parents for the steps of one MMA group,
+  // [8 warps][NG steps][8 grand-parents] float4 (chain_pre)
+  static constexpr int oCb = oPark + (kDeferChain ? 8 * CH * 32 * 4 : 0);
+  static constexpr int oBar = oCb + (kDeferChain ? 8 * NG * 8 * 16 : 0);  // mbarriers: MMA groups 0, 1; ready 0, 1
   static constexpr int oSlot = oBar + 32;
   static constexpr size_t kSmem = oSlot + 16;
 };
@@ -119,6 +122,7 @@ __global__ void __launch_bounds__(kBlock, 1)
   float(*red)[8][CH][D] = reinterpret_cast<float(*)[8][CH][D]>(sm + Q_::oRed);
   auto isig = [&](int db) { return reinterpret_cast<float*>(sm + Q_::oSig) + db * CH; };
   float* park = reinterpret_cast<float*>(sm + Q_::oPark);
+  float4* cbuf = reinterpret_cast<float4*>(sm + Q_::oCb) + (threadIdx.x >> 5) * NG * 8;  // this warp's chain values
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + Q_::oBar);
   uint32_t* slot = reinterpret_cast<uint32_t*>(sm + Q_::oSlot);
 
@@ -246,10 +250,17 @@ __global__ void __launch_bounds__(kBlock, 1)
     stage(nchunks - 1, 0);
     if (nchunks > 1) stage(nchunks - 2, 1);
   }
-  float sc[NC], lc[NC];  // chain values S_j and (partial) adjoints; a node is seeded once (the owner)
+  // chain values S_j and (partial) adjoints; a node is seeded once (the owner).  Depth 4: sc holds
+  // the chain of the grand-parent this lane walks in chain_pre, (gp & ~7) + (lane & 7)
+  float sc[NC], lc[NC];
 #pragma unroll
   for (int k = 0; k < NC; ++k) {
-    sc[k] = srow[chain_index(k)];
+    if constexpr (Q_::kDeferChain) {
+      const int gps = (gp & ~7) + (lane & 7);
+      sc[k] = srow[k == 0 ? Q_::off(1) + gps / D : Q_::off(2) + gps];
+    } else {
+      sc[k] = srow[chain_index(k)];
+    }
     const bool owner = q == 0 && gp % trunc::ipow(D, NC - 1 - k) == 0;
     lc[k] = owner ? grow[chain_index(k)] : 0.f;
   }
@@ -291,6 +302,7 @@ __global__ void __launch_bounds__(kBlock, 1)
     }
   const float s1 = tcu::pow2_scale(amax1), s2 = tcu::pow2_scale(amax2);
   const float inv_s1 = 1.f / s1, inv_s2 = 1.f / s2;  // exact: powers of two
+  const float ninv_s2 = -inv_s2, inv_s1h = 0.5f * inv_s1;
   if (!producer) {
 #pragma unroll
     for (int g = 0; g < 4; ++g) {  // A1 row (tile mt0 + g) = parent gp.(4q+g), K = leaf letter z (zero-padded)
@@ -374,37 +386,43 @@ __global__ void __launch_bounds__(kBlock, 1)
   // one reverse step s of the current chunk; rr = the TMEM products of step s (D1 then D2)
   // a step's increments (its quad's 4 letters, the chain letters) and 1/sigma, fetched one step
   // ahead so the next step's shared loads sit above this step's parked-sum store
+  // (depth 4: the chain values come precomputed per step from chain_pre instead, cb)
   struct Inc {
     float4 y;
     float dc[NC];
     float is;
+    float4 cb;  // depth 4: (Tr(gp,3) / sigma, T(gp,3), T(gp,4) / (2 sigma), 1 / sigma)
   };
-  auto fetch = [&](int s, const float* dl, const float* isg) {
+  auto fetch = [&](int s, const float* dl, const float* isg, int lo) {
     const float* row = dl + s * D;
     Inc in;
     in.y = *reinterpret_cast<const float4*>(row + 4 * q);
+    if constexpr (Q_::kDeferChain) {
+      in.cb = cbuf[(s - lo) * 8 + (lane >> 2)];
+    } else {
 #pragma unroll
-    for (int k = 0; k < NC; ++k) in.dc[k] = row[cl[k]];
-    in.is = isg[s];
+      for (int k = 0; k < NC; ++k) in.dc[k] = row[cl[k]];
+      in.is = isg[s];
+    }
     return in;
   };
   // a step's letter sums before the cross-lane reduction: the reduction of step s is issued after
   // the arithmetic of step s-1 (source order), so its shuffle latency overlaps that arithmetic
   struct Sums {
     float v[4], gc[NC];  // depth 4: gc[0], gc[1] = this lane's parent-adjoint sums T1, T2 (see park)
-    float x;             // depth 4: the lane's chain input for the park (d1, S_j(level 1) or d0)
   };
   float* park_w = park + warp * CH * 32;
   auto reduce = [&](Sums& u, int s, float(*redw)[D]) {
     float* v = u.v;
     if constexpr (Q_::kDeferChain) {
       // park the grand-parent's T1 = Tbar(gp, 3), T2 = Tbar(gp, 4) contributions (summed over the quad:
-      // transposing over lane bit 0, then plain over bit 1) and S_j(level 1) for the deferred sweep
+      // transposing over lane bit 0, then plain over bit 1) for the deferred sweep (quad lanes 2, 3
+      // of the park row hold the chain inputs, written by chain_pre)
       const bool b0 = (lane & 1) != 0;
       float keep = b0 ? u.gc[1] : u.gc[0];
       keep += __shfl_xor_sync(0xffffffffu, b0 ? u.gc[0] : u.gc[1], 1);
       keep += __shfl_xor_sync(0xffffffffu, keep, 2);
-      park_w[s * 32 + lane] = (lane & 2) ? u.x : keep;
+      if (!(lane & 2)) park_w[s * 32 + lane] = keep;
     } else {
       // the quad group's partial chain terms -> full per grand-parent, added at the lane of their letter
 #pragma unroll
@@ -435,22 +453,15 @@ __global__ void __launch_bounds__(kBlock, 1)
   };
   auto step = [&](const Inc& in, const uint32_t (&rr)[8]) -> Sums {
     const float dy[4] = {in.y.x, in.y.y, in.y.z, in.y.w};
-    const float is = in.is;
-    float trN1, tN1, tN;
+    float is, trN1, tN1, tN;
     float tp[NC][N + 1];  // forward partials T(chain_k, m) from S_j (m = k+1 .. N)
-    if constexpr (NC == 2) {
-      // depth 4 written out (the generic loops below cost ~3% at config 5)
-      const float d0 = in.dc[0], d1 = in.dc[1];
-      const float r0_3 = sc[0] - d0 * (1.f / 3.f);
-      trN1 = fmaf(-0.5f * d1, r0_3, sc[1]);  // Tr(gp, 3): the exp(-dX) partial
-      const float nsc1 = fmaf(-d1, sc[0] - 0.5f * d0, sc[1]);
-      sc[0] = sc[0] - d0;
-      sc[1] = nsc1;
-      tp[0][2] = fmaf(0.5f, d0, sc[0]);
-      tp[0][3] = fmaf(1.f / 3.f, d0, sc[0]);
-      tp[0][4] = fmaf(0.25f, d0, sc[0]);
-      tN1 = fmaf(0.5f * d1, tp[0][3], sc[1]);         // T(gp, 3)
-      tN = fmaf(d1 * (1.f / 3.f), tp[0][4], sc[1]);   // T(gp, 4)
+    float pq, gq, gt;     // the MMA products carry the operand scales: D1 = Tbar(u, N) / k1, D2 = Q / k2
+    if constexpr (Q_::kDeferChain) {
+      is = in.cb.w;
+      tN1 = in.cb.y;
+      pq = in.cb.x * ninv_s2;  // -Tr(gp,3) k2
+      gq = in.cb.z * inv_s2;   // T(gp,4)/2 k2
+      gt = in.cb.z * inv_s1;   // T(gp,4)/2 k1
     } else {
       // (a) reconstruct S_j = S_{j+1} (x) exp(-dX_j) on the chain: partials of the exp(-dX) step
       // (targets up to N-1; Tr(gp, N-1) drives the parents' and P's reconstruction)
@@ -479,10 +490,13 @@ __global__ void __launch_bounds__(kBlock, 1)
       }
       tN1 = tp[NC - 1][N - 1];  // T(gp, N-1)
       tN = tp[NC - 1][N];       // T(gp, N)
+      is = in.is;
+      const float k2 = inv_s2 * is;
+      pq = -trN1 * k2;
+      gq = 0.5f * tN * k2;
+      gt = 0.5f * tN * (inv_s1 * is);
     }
-    // the MMA products carry the operand scales: D1 = Tbar(u, N) / k1, D2 = Q / k2
-    const float k1 = inv_s1 * is, k2 = inv_s2 * is;
-    const float pq = -trN1 * k2, gq = 0.5f * tN * k2, gt = 0.5f * tN * k1;
+    const float k1 = inv_s1 * is;
     Sums out;
     float* v = out.v;
     float tbp1 = 0.f, tbp2u = 0.f;  // Tbar(gp, N-1), Tbar(gp, N) / k1 from the parents
@@ -500,16 +514,13 @@ __global__ void __launch_bounds__(kBlock, 1)
       v[i] = fmaf(gt, Du, fmaf(lm, tN1, fmaf(gq, Di, P[i])));
       lm_[i] = fmaf(Du, k1, lm);
     }
-    const float tbp2 = 0.5f * k1 * tbp2u;
+    const float tbp2 = (inv_s1h * is) * tbp2u;
     // chain, deepest first (trunc_backward_kernel (c)): tbc[m] = Tbar contributed by the child
     if constexpr (Q_::kDeferChain) {
       // the chain's reverse is a pure sink (its adjoints feed only the chain letters' gradients):
       // swept once per grand-parent after the chunk (chain_sweep), from the parked T1, T2, S_j
       out.gc[0] = tbp1;
       out.gc[1] = tbp2;
-      // quad lane 2 parks d1 (its grand-parent's letter), lane 3 the warp-common S_j(la) (even
-      // grand-parents) or d0 (odd ones)
-      out.x = (lane & 1) ? ((lane & 4) ? in.dc[0] : sc[0]) : in.dc[1];
     } else {
       float tbc[N + 1];
 #pragma unroll
@@ -537,6 +548,68 @@ __global__ void __launch_bounds__(kBlock, 1)
       }
     }
     return out;
+  };
+
+  // Depth 4: the chain values of the warp's 8 grand-parents for the steps lo..hi of one MMA group,
+  // computed before the group's steps (under its MMA wait) instead of by every quad lane per step.
+  // Lane (g = lane & 7, quarter qq = lane >> 3) walks grand-parent (gp & ~7) + g over steps
+  // lo+4qq+3 .. lo+4qq; the state entering its quarter comes from a suffix scan of the quarter maps
+  //   (S1, S2) -> (S1 - A, S2 - S1 Bs + C),  A = sum d0, Bs = sum d1, C = sum d1 (a + d0 / 2)
+  // (S1 = S_j(la), S2 = S_j(gp), a = the quarter's d0 after the step), composed upper then lower as
+  //   (A_u + A_l, Bs_u + Bs_l, C_u + C_l + A_u Bs_l).
+  // Writes cbuf[s - lo][g] for the steps and the park row's chain inputs (quad lanes 2, 3: d1, and
+  // S_j(la) for even / d0 for odd grand-parents), and carries sc below the group.
+  auto chain_pre = [&](const float* dl, const float* isg, int lo, int hi) {
+    if constexpr (Q_::kDeferChain) {
+      __syncwarp();  // the previous group's steps have read cbuf
+      const int g = lane & 7, qq = lane >> 3;
+      const int gps = (gp & ~7) + g, c0 = gps / D, c1 = gps % D;
+      float d0v[4], d1v[4], A = 0.f, Bs = 0.f, C = 0.f;
+#pragma unroll
+      for (int i = 3; i >= 0; --i) {
+        const int st = lo + 4 * qq + i;
+        d0v[i] = st <= hi ? dl[st * D + c0] : 0.f;
+        d1v[i] = st <= hi ? dl[st * D + c1] : 0.f;
+        C = fmaf(d1v[i], A + 0.5f * d0v[i], C);
+        A += d0v[i];
+        Bs += d1v[i];
+      }
+#pragma unroll
+      for (int off = 8; off <= 16; off *= 2) {  // inclusive suffix scan over the quarters
+        const float oA = __shfl_down_sync(0xffffffffu, A, off);
+        const float oB = __shfl_down_sync(0xffffffffu, Bs, off);
+        const float oC = __shfl_down_sync(0xffffffffu, C, off);
+        if (qq + off / 8 <= 3) {
+          C = fmaf(oA, Bs, C + oC);
+          A += oA;
+          Bs += oB;
+        }
+      }
+      float eA = __shfl_down_sync(0xffffffffu, A, 8);  // exclusive: the quarters above this one
+      float eB = __shfl_down_sync(0xffffffffu, Bs, 8);
+      float eC = __shfl_down_sync(0xffffffffu, C, 8);
+      if (qq == 3) eA = eB = eC = 0.f;
+      float s0 = sc[0] - eA, s1 = fmaf(-sc[0], eB, sc[1] + eC);
+#pragma unroll
+      for (int i = 3; i >= 0; --i) {
+        const int st = lo + 4 * qq + i;
+        const float d0 = d0v[i], d1 = d1v[i];
+        const float trN1 = fmaf(-0.5f * d1, s0 - d0 * (1.f / 3.f), s1);  // Tr(gp, 3): the exp(-dX) partial
+        const float ns1 = fmaf(-d1, s0 - 0.5f * d0, s1);
+        s0 = s0 - d0;
+        s1 = ns1;
+        const float tN1 = fmaf(0.5f * d1, fmaf(1.f / 3.f, d0, s0), s1);        // T(gp, 3)
+        const float tN = fmaf(d1 * (1.f / 3.f), fmaf(0.25f, d0, s0), s1);      // T(gp, 4)
+        if (st <= hi) {
+          const float is = isg[st];
+          cbuf[(st - lo) * 8 + g] = make_float4(trN1 * is, tN1, 0.5f * tN * is, is);
+          *reinterpret_cast<float2*>(park_w + st * 32 + 4 * g + 2) = make_float2(d1, (g & 1) ? d0 : s0);
+        }
+      }
+      sc[0] = __shfl_sync(0xffffffffu, s0, g);  // the state below the group: quarter 0's walk
+      sc[1] = __shfl_sync(0xffffffffu, s1, g);
+      __syncwarp();
+    }
   };
 
   // chunk epilogue: fixed-order sum over the 8 compute warps' parked letter sums of chunk c (buffer
@@ -670,6 +743,7 @@ __global__ void __launch_bounds__(kBlock, 1)
 #pragma unroll 1
       for (int h = 1; h >= 0; --h) {
         const int lo = NG * h, hi = (cs < NG * (h + 1) ? cs : NG * (h + 1)) - 1;
+        if (hi >= lo) chain_pre(dl, is, lo, hi);
         tcu::mbar_wait(&mbar[h], (uint32_t)(k & 1));  // group h's products are in TMEM
         tcu::fence_after();
         if (hi >= lo) {
@@ -693,16 +767,16 @@ __global__ void __launch_bounds__(kBlock, 1)
           uint32_t ra[8], rb[8], rc[8], rd[8];
           Inc ia, ib, ic, id;
           load1(ra, hi);
-          ia = fetch(hi, dl, is);
+          ia = fetch(hi, dl, is, lo);
           int s = hi - 1;
           auto issue_next = [&](uint32_t (&rlo)[8], uint32_t (&rhi)[8], Inc& ilo, Inc& ihi, int top) {
             if (top - 1 >= lo) {
               load2(rlo, rhi, top - 1);
-              ihi = fetch(top, dl, is);
-              ilo = fetch(top - 1, dl, is);
+              ihi = fetch(top, dl, is, lo);
+              ilo = fetch(top - 1, dl, is, lo);
             } else if (top >= lo) {
               load1(rhi, top);
-              ihi = fetch(top, dl, is);
+              ihi = fetch(top, dl, is, lo);
             }
           };
           issue_next(rc, rd, ic, id, s);
