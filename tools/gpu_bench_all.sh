@@ -4,7 +4,7 @@
 O=gpurun_out/bench_all; mkdir -p $O
 run() { n=$1; shift; timeout 900 python bench.py "$@" > $O/$n.json 2> $O/$n.err; tail -1 $O/$n.json | cut -c1-200; }
 run c1 --config c1 --steps 6000 --warmup 5
-run c2 --config c2 --steps 80 --warmup 3
+run c2 --config c2 --steps 140 --warmup 3
 run c3 --config c3 --steps 300 --warmup 5
 run c4 --config c4 --steps 12 --warmup 3
 run p1 --config p1 --steps 2000 --warmup 5
