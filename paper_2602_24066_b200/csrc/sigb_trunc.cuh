@@ -290,10 +290,13 @@ __device__ __forceinline__ void chen_step(State<T, D, N, G>& st, const StepIncr<
   const T tN = NC > 0 ? tch[NC > 0 ? NC - 1 : 0][N] : T(1);
 #pragma unroll
   for (int k = 0; k < NC; ++k) st.ch[k] = tch[k][k + 1];
+  // dX/2 . T(gp, N) as dX . (T(gp, N)/2): one scaling per step instead of one per parent (exact, so
+  // bitwise the same)
+  const T tNh = tN * inv<T, 2>();
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     if constexpr (Leaves) {
-      const T tm = fma(in.dy[g] * inv<T, 2>(), tN, st.mid[g]);  // T(u_g, N)
+      const T tm = fma(in.dy[g], tNh, st.mid[g]);  // T(u_g, N)
       if constexpr (sizeof(T) == 4 && D % 2 == 0) {
         // packed f32x2 FMAs: half the issue slots for the leaf level (the FMA
         // pipe still does one lane-FMA per cycle, see tools/ubench_fma.cu)
@@ -819,6 +822,7 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS, (TC || (sizeof(T) == 4 
       chain_partials<T, D, N, G>(st, in, tch);
       const T tN1 = NC > 0 ? tch[NCc - 1][N - 1] : T(1);
       const T tN = NC > 0 ? tch[NCc - 1][N] : T(1);
+      const T tNh = tN * inv<T, 2>();  // halvings folded per step (exact: bitwise the same results)
       // (c) reverse: leaves, mids, chain
       T gl[D];
 #pragma unroll
@@ -837,7 +841,7 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS, (TC || (sizeof(T) == 4 
       }
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        const T tm = fma(in.dy[g] * inv<T, 2>(), tN, st.mid[g]);  // T(u_g, N)
+        const T tm = fma(in.dy[g], tNh, st.mid[g]);  // T(u_g, N)
         T tb0 = T(0), tb1 = T(0);
         if constexpr (TC) {
           const float2 tm2 = make_float2(tm, tm);
@@ -877,8 +881,8 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS, (TC || (sizeof(T) == 4 
         const T tb = TC ? tb0 : tb0 + tb1;  // Tbar(u_g, N)
         const T lm = lam.mid[g];  // Tbar(u_g, N-1)
         tbp1 = fma(in.dy[g], lm, tbp1);
-        tbp2 = fma(in.dy[g] * inv<T, 2>(), tb, tbp2);
-        gm[g] = fma(lm, tN1, tb * tN * inv<T, 2>());
+        tbp2 = fma(in.dy[g], tb, tbp2);  // halved after the loop
+        gm[g] = fma(lm, tN1, tb * tNh);
         lam.mid[g] = lm + tb;
       }
       // mids' gradient terms join the leaf letters (letter q*G + g).  A separate
@@ -902,7 +906,7 @@ __global__ void __launch_bounds__(Cfg<D, N, G>::THREADS, (TC || (sizeof(T) == 4 
 #pragma unroll
         for (int m = 0; m <= N; ++m) tbc[m] = T(0);
         tbc[N - 1] = tbp1;
-        tbc[N] = tbp2;
+        tbc[N] = tbp2 * inv<T, 2>();
 #pragma unroll
         for (int k = NC - 1; k >= 0; --k) {
           const int lv = k + 1;

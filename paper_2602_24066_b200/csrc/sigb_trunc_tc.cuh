@@ -214,9 +214,10 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
           const float tN = NC > 0 ? tch[NC > 0 ? NC - 1 : 0][N] : 1.f;
 #pragma unroll
           for (int k = 0; k < NC; ++k) ch[k] = tch[k][k + 1];
+          const float tNh = 0.5f * tN;  // dX/2 . T(gp, N) as dX . (T(gp, N)/2): exact, one scaling per step
 #pragma unroll
           for (int g = 0; g < G; ++g) {
-            const float tm = fmaf(in.dy[g] * 0.5f, tN, mid[g]);  // T(u_g, N): the leaves' multiplier
+            const float tm = fmaf(in.dy[g], tNh, mid[g]);  // T(u_g, N): the leaves' multiplier
             mid[g] = fmaf(in.dy[g], tN1, mid[g]);
             const float h = tf32_hi(tm);
             ah[g][s] = h;
