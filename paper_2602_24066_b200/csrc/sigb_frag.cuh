@@ -115,10 +115,11 @@ __device__ __forceinline__ void chen_step(FState<T, NC, G, K>& st, const FIncr<T
   const T tN = tch[NC - 1][NV];
 #pragma unroll
   for (int k = 0; k < NC; ++k) st.ch[k] = tch[k][k + 1];
+  const T tNh = tN * T(0.5);  // dX/2 . T(anchor, NV) as dX . (T/2): exact, one scaling per step
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     if constexpr (Leaves) {
-      const T tm = fma(in.dy[g] * T(0.5), tN, st.mid[g]);  // T(mid_g, NV)
+      const T tm = fma(in.dy[g], tNh, st.mid[g]);  // T(mid_g, NV)
       if constexpr (sizeof(T) == 4) {
         // packed f32x2 FMAs for pairs of leaves (half the issue slots)
         const float2 tm2 = make_float2(tm, tm);
@@ -363,6 +364,7 @@ __global__ void __launch_bounds__(kTPB) frag_backward_kernel(FragDev fd, const T
       chain_partials<T, NC, G, K>(st, in, tch);
       const T tN1 = tch[NC - 1][NV - 1];
       const T tN = tch[NC - 1][NV];
+      const T tNh = tN * T(0.5);  // halvings folded per step (exact: bitwise the same results)
       // (c) reverse: leaves, mids, anchor leaves, chain
       T gl[K];
 #pragma unroll
@@ -371,7 +373,7 @@ __global__ void __launch_bounds__(kTPB) frag_backward_kernel(FragDev fd, const T
       T tbp1 = T(0), tbp2 = T(0);  // Tbar(anchor, NV-1), Tbar(anchor, NV)
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        const T tm = fma(in.dy[g] * T(0.5), tN, st.mid[g]);
+        const T tm = fma(in.dy[g], tNh, st.mid[g]);
         T tb = T(0);
         if constexpr (sizeof(T) == 4 && K >= 2) {
           // packed f32x2: leaf pairs; the adjoint dot product keeps two partial sums
@@ -399,8 +401,8 @@ __global__ void __launch_bounds__(kTPB) frag_backward_kernel(FragDev fd, const T
         }
         const T lm = lam.mid[g];
         tbp1 = fma(in.dy[g], lm, tbp1);
-        tbp2 = fma(in.dy[g] * T(0.5), tb, tbp2);
-        gm[g] = fma(lm, tN1, tb * tN * T(0.5));
+        tbp2 = fma(in.dy[g], tb, tbp2);  // halved below
+        gm[g] = fma(lm, tN1, tb * tNh);
         lam.mid[g] = lm + tb;
       }
       T ga[K];
@@ -415,7 +417,7 @@ __global__ void __launch_bounds__(kTPB) frag_backward_kernel(FragDev fd, const T
 #pragma unroll
         for (int m = 0; m <= NV; ++m) tbc[m] = T(0);
         tbc[NV - 1] = tbp1;
-        tbc[NV] = tbp2;
+        tbc[NV] = tbp2 * T(0.5);
 #pragma unroll
         for (int k = NC - 1; k >= 0; --k) {
           const int lv = k + 1;

@@ -1,0 +1,7 @@
+#!/bin/bash
+# full GPU suite on the in-tree build, then A/B of two builds on c4 (fragment kernels)
+O=gpurun_out/ab; mkdir -p $O
+timeout 1200 python -m pytest tests -m gpu -x -q > $O/pytest.txt 2>&1; echo "rc=$?" >> $O/pytest.txt; tail -2 $O/pytest.txt
+for r in 1 2 3; do for L in "$@"; do
+  SIGB_LIB_PATH=$L timeout 300 python tools/time_bwd.py 1024 c4
+done; done
