@@ -671,14 +671,15 @@ __global__ void __launch_bounds__(kBlock, 1)
       float cg[8], csum[8];
 #pragma unroll
       for (int i = 7; i >= 0; --i) {
-        const float tp2 = fmaf(0.5f, d0[i], s0[i]), tp3 = fmaf(1.f / 3.f, d0[i], s0[i]);
-        const float tp4 = fmaf(0.25f, d0[i], s0[i]);
+        // with T(la, m) = S + d0/m the terms regroup into u = n2 + n3/2 + n4/3 and
+        // w = n2/2 + n3/6 + n4/12:  gl[cl1] += S u + d0 w,  c2 + c3 + c4 = d1 u,  c2/2 + c3/3 + c4/4 = d1 w
         const float n3 = t1[i], n4 = t2[i];
-        const float gc1 = fmaf(n2, tp2, fmaf(0.5f * n3, tp3, (1.f / 3.f) * n4 * tp4));
-        const float c2 = d1[i] * n2, c3 = 0.5f * d1[i] * n3, c4 = (1.f / 3.f) * d1[i] * n4;
+        const float u = fmaf(0.5f, n3, fmaf(1.f / 3.f, n4, n2));
+        const float w = fmaf(0.5f, n2, fmaf(1.f / 6.f, n3, (1.f / 12.f) * n4));
+        const float gc1 = fmaf(s0[i], u, d0[i] * w);
         n2 = n2 + n3 + n4;
-        cg[i] = fmaf(0.5f, c2, fmaf(1.f / 3.f, c3, 0.25f * c4));
-        csum[i] = c2 + c3 + c4;
+        cg[i] = d1[i] * w;
+        csum[i] = d1[i] * u;
         C += csum[i];
         const int st = 8 * qq + i;
         if (st < cs) redw[st][c1] += gc1;
