@@ -300,9 +300,19 @@ __global__ void __launch_bounds__(kBlock, 1)
       const float4 t = lchunk(4 * q + g, j);
       amax1 = fmaxf(fmaxf(amax1, fmaxf(fabsf(t.x), fabsf(t.y))), fmaxf(fabsf(t.z), fabsf(t.w)));
     }
+  // depth 4: one scale per grand-parent (the quad's max over both operands), so chain_pre can fold
+  // it into the step's chain values; elsewhere one per thread and operand
+  if constexpr (Q_::kDeferChain) {
+    amax1 = fmaxf(amax1, amax2);
+    amax1 = fmaxf(amax1, __shfl_xor_sync(0xffffffffu, amax1, 1));
+    amax1 = fmaxf(amax1, __shfl_xor_sync(0xffffffffu, amax1, 2));
+    amax2 = amax1;
+  }
   const float s1 = tcu::pow2_scale(amax1), s2 = tcu::pow2_scale(amax2);
   const float inv_s1 = 1.f / s1, inv_s2 = 1.f / s2;  // exact: powers of two
-  const float ninv_s2 = -inv_s2, inv_s1h = 0.5f * inv_s1;
+  const float inv_s1h = 0.5f * inv_s1;
+  // the scale of the grand-parent this lane walks in chain_pre, (gp & ~7) + (lane & 7)
+  const float inv_sp = __shfl_sync(0xffffffffu, inv_s1, 4 * (lane & 7));
   if (!producer) {
 #pragma unroll
     for (int g = 0; g < 4; ++g) {  // A1 row (tile mt0 + g) = parent gp.(4q+g), K = leaf letter z (zero-padded)
@@ -453,15 +463,16 @@ __global__ void __launch_bounds__(kBlock, 1)
   };
   auto step = [&](const Inc& in, const uint32_t (&rr)[8]) -> Sums {
     const float dy[4] = {in.y.x, in.y.y, in.y.z, in.y.w};
-    float is, trN1, tN1, tN;
+    float is = 0.f, trN1, tN1, tN;
     float tp[NC][N + 1];  // forward partials T(chain_k, m) from S_j (m = k+1 .. N)
-    float pq, gq, gt;     // the MMA products carry the operand scales: D1 = Tbar(u, N) / k1, D2 = Q / k2
+    float pq, gq, gt, k1;  // the MMA products carry the operand scales: D1 = Tbar(u, N) / k1, D2 = Q / k2
     if constexpr (Q_::kDeferChain) {
-      is = in.cb.w;
+      // chain_pre folded the grand-parent's scale (k1 = k2 = 1 / (s sigma)): cb = (-Tr(gp,3) k, T(gp,3),
+      // T(gp,4)/2 k, k)
+      pq = in.cb.x;
       tN1 = in.cb.y;
-      pq = in.cb.x * ninv_s2;  // -Tr(gp,3) k2
-      gq = in.cb.z * inv_s2;   // T(gp,4)/2 k2
-      gt = in.cb.z * inv_s1;   // T(gp,4)/2 k1
+      gq = gt = in.cb.z;
+      k1 = in.cb.w;
     } else {
       // (a) reconstruct S_j = S_{j+1} (x) exp(-dX_j) on the chain: partials of the exp(-dX) step
       // (targets up to N-1; Tr(gp, N-1) drives the parents' and P's reconstruction)
@@ -494,9 +505,9 @@ __global__ void __launch_bounds__(kBlock, 1)
       const float k2 = inv_s2 * is;
       pq = -trN1 * k2;
       gq = 0.5f * tN * k2;
-      gt = 0.5f * tN * (inv_s1 * is);
+      k1 = inv_s1 * is;
+      gt = 0.5f * tN * k1;
     }
-    const float k1 = inv_s1 * is;
     Sums out;
     float* v = out.v;
     float tbp1 = 0.f, tbp2u = 0.f;  // Tbar(gp, N-1), Tbar(gp, N) / k1 from the parents
@@ -514,7 +525,8 @@ __global__ void __launch_bounds__(kBlock, 1)
       v[i] = fmaf(gt, Du, fmaf(lm, tN1, fmaf(gq, Di, P[i])));
       lm_[i] = fmaf(Du, k1, lm);
     }
-    const float tbp2 = (inv_s1h * is) * tbp2u;
+    // Tbar(gp, N): depth 4 parks it doubled (the sweep halves it once per grand-parent)
+    const float tbp2 = Q_::kDeferChain ? k1 * tbp2u : (inv_s1h * is) * tbp2u;
     // chain, deepest first (trunc_backward_kernel (c)): tbc[m] = Tbar contributed by the child
     if constexpr (Q_::kDeferChain) {
       // the chain's reverse is a pure sink (its adjoints feed only the chain letters' gradients):
@@ -602,7 +614,8 @@ __global__ void __launch_bounds__(kBlock, 1)
         const float tN = fmaf(d1 * (1.f / 3.f), fmaf(0.25f, d0, s0), s1);      // T(gp, 4)
         if (st <= hi) {
           const float is = isg[st];
-          cbuf[(st - lo) * 8 + g] = make_float4(trN1 * is, tN1, 0.5f * tN * is, is);
+          const float k = inv_sp * is;
+          cbuf[(st - lo) * 8 + g] = make_float4(-trN1 * k, tN1, 0.5f * tN * k, k);
           *reinterpret_cast<float2*>(park_w + st * 32 + 4 * g + 2) = make_float2(d1, (g & 1) ? d0 : s0);
         }
       }
@@ -649,7 +662,7 @@ __global__ void __launch_bounds__(kBlock, 1)
         float4 pk = make_float4(0.f, 0.f, 0.f, 0.f);
         if (st < cs) pk = *reinterpret_cast<const float4*>(park_w + st * 32 + 4 * g);
         const float other = __shfl_xor_sync(0xffffffffu, pk.w, 1);
-        t1[i] = pk.x; t2[i] = pk.y; d1[i] = pk.z;
+        t1[i] = pk.x; t2[i] = 0.5f * pk.y; d1[i] = pk.z;  // T2 was parked doubled
         s0[i] = (g & 1) ? other : pk.w;
         d0[i] = (g & 1) ? pk.w : other;
         A += t1[i] + t2[i];
