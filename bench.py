@@ -700,9 +700,10 @@ def run_ours(args) -> None:
                        "length": L, "d": d, "W": W, "sum_word_len": sl,
                        "parallelism": f"dp{world}: batch-sharded, no collective in fwd/bwd",
                        "l2": l2_note,
-                       "kernels": {1: "truncated register-resident", 2: "fragment register-resident",
-                                   3: "level-slot", 4: "word-set generated (NVRTC)"}.get(
-                           plan.kernel_kind, "level-synchronous trie")},
+                       "kernels": "%s: fwd %s, bwd %s" % (
+                           {1: "truncated", 2: "fragment", 4: "word-set generated (NVRTC)"}.get(
+                               plan.kernel_kind, "level-synchronous trie"),
+                           kf_name, kb_name)},
             "fwd": {"value": fwd_value, "unit": "paths/s", "ms_per_step": fwd_ms / args.steps},
             "roofline": dominant, "roofline_fwd": roof_f if dominant is not roof_f else roof_b,
             "cpu_baseline": cpu, "e2e": e2e, "e2e_fwd": e2e_fwd, "e2e_dropin_fwd_bwd": e2e_dropin, "gather": gather,
