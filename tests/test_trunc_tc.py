@@ -58,34 +58,41 @@ def test_tc_forward_deterministic(monkeypatch):
     assert torch.equal(a, b)
 
 
-# -- backward: the leaf term tb = Lambda . dX on the tensor cores (TcBwd, sigb_trunc.cuh) ----------
+# -- backward on the tensor cores: SIGB_TRUNC_TC_BWD = "2" the P/Q kernel (sigb_trunc_pq.cuh, the
+# default), "1" the intermediate kernel with only tb = Lambda . dX on tcgen05 (TcBwd, sigb_trunc.cuh;
+# d = 16 only -- d = 8 falls back to the CUDA cores), "0" the CUDA-core kernel ------------------------
+
+BWD_MODES = ["2", "1"]
 
 
-def _autograd(X, ws, g, tc_bwd, monkeypatch):
-    monkeypatch.setenv("SIGB_TRUNC_TC_BWD", "1" if tc_bwd else "0")
+def _autograd(X, ws, g, mode, monkeypatch):
+    monkeypatch.setenv("SIGB_TRUNC_TC_BWD", mode)
     Xt = torch.from_numpy(X).cuda().requires_grad_(True)
     S = sk.signature(Xt, ws)
     S.backward(torch.from_numpy(g).cuda())
     return Xt.grad.cpu().numpy()
 
 
+@pytest.mark.parametrize("mode", BWD_MODES)
 @pytest.mark.parametrize("d,N", [(16, 4), (8, 5)])
-@pytest.mark.parametrize("L", [2, 3, 17, 33, 34, 65, 200])
-def test_tc_backward_matches_oracle(d, N, L, monkeypatch):
-    """Chunk edges (M < 32, M = 32, M = 33, ragged last chunk) against the fp64 oracle and the
-    CUDA-core backward, for both P/Q instantiations (config 5 and config 2 sets)."""
+@pytest.mark.parametrize("L", [2, 3, 17, 18, 33, 34, 49, 65, 200])
+def test_tc_backward_matches_oracle(d, N, L, mode, monkeypatch):
+    """Chunk and MMA-group edges (M = 1, M < 16, M = 16 / 17 (second group empty / one step), M = 32,
+    M = 33, M = 48, ragged last chunk) against the fp64 oracle and the CUDA-core backward, for both
+    P/Q instantiations (config 5 and config 2 sets)."""
     ws = sk.build_truncated(d, N)
     B = 3
     X = brownian(40 + L, B, L, d).astype(np.float32)
     g = np.random.default_rng(L).standard_normal((B, len(ws))).astype(np.float32)
-    dX = _autograd(X, ws, g, True, monkeypatch)
+    dX = _autograd(X, ws, g, mode, monkeypatch)
     _, dref = ora.backward(X.astype(np.float64), ws.codes, ws.lengths, d, g.astype(np.float64))
     assert ora.rel_err(dX, dref) <= TOL32
-    assert ora.rel_err(dX, _autograd(X, ws, g, False, monkeypatch)) <= TOL32
+    assert ora.rel_err(dX, _autograd(X, ws, g, "0", monkeypatch)) <= TOL32
 
 
+@pytest.mark.parametrize("mode", BWD_MODES)
 @pytest.mark.parametrize("d,N", [(16, 4), (8, 5)])
-def test_tc_backward_scaled_inputs(d, N, monkeypatch):
+def test_tc_backward_scaled_inputs(d, N, mode, monkeypatch):
     """Power-of-two operand scaling: upstream rows spanning 2^-30..2^30, a path scaled by 1e4,
     one by 1e-4, a constant stretch (zero increments), a zero upstream path."""
     ws = sk.build_truncated(d, N)
@@ -100,19 +107,20 @@ def test_tc_backward_scaled_inputs(d, N, monkeypatch):
     g *= np.exp2(rng.integers(-30, 31, size=(B, len(ws))))
     g[4] = 0.0
     g = g.astype(np.float32)
-    dX = _autograd(X, ws, g, True, monkeypatch)
+    dX = _autograd(X, ws, g, mode, monkeypatch)
     _, dref = ora.backward(X.astype(np.float64), ws.codes, ws.lengths, d, g.astype(np.float64))
     for b in range(B):
         assert ora.rel_err(dX[b], dref[b]) <= TOL32, b
     assert not np.any(dX[4])
 
 
-def test_tc_backward_deterministic(monkeypatch):
+@pytest.mark.parametrize("mode", BWD_MODES)
+def test_tc_backward_deterministic(mode, monkeypatch):
     ws = sk.build_truncated(16, 4)
     X = brownian(81, 9, 100, 16).astype(np.float32)
     g = np.random.default_rng(82).standard_normal((9, len(ws))).astype(np.float32)
-    a = _autograd(X, ws, g, True, monkeypatch)
-    b = _autograd(X, ws, g, True, monkeypatch)
+    a = _autograd(X, ws, g, mode, monkeypatch)
+    b = _autograd(X, ws, g, mode, monkeypatch)
     assert np.array_equal(a, b)
 
 
@@ -149,13 +157,14 @@ def test_tensor_core_switch(monkeypatch):
         assert ora.rel_err(dX, dref) <= TOL32
 
 
+@pytest.mark.parametrize("mode", BWD_MODES)
 @pytest.mark.parametrize("d,N", [(16, 4), (8, 5)])
-def test_tc_backward_epsilon_column(d, N, monkeypatch):
+def test_tc_backward_epsilon_column(d, N, mode, monkeypatch):
     """include_empty: the upstream carries a leading epsilon column (g_col0 = 1), so the staged leaf
     block is not 16-byte aligned and the kernel takes its 4-byte copies."""
     ws = sk.build_truncated(d, N, include_empty=True)
     X = brownian(95, 3, 41, d).astype(np.float32)
     g = np.random.default_rng(96).standard_normal((3, len(ws) + 1)).astype(np.float32)
-    dX = _autograd(X, ws, g, True, monkeypatch)
+    dX = _autograd(X, ws, g, mode, monkeypatch)
     _, dref = ora.backward(X.astype(np.float64), ws.codes, ws.lengths, d, g[:, 1:].astype(np.float64))
     assert ora.rel_err(dX, dref) <= TOL32
