@@ -319,8 +319,9 @@ extern "C" int sigb_backward_workspace_size(const sigb_plan* plan, int dtype, in
     *bytes = frag::backward_workspace(plan, dtype, B, L);
     return SIGB_OK;
   }
-  if (use_frag(plan) && ckpt_stride == 0) {
-    *bytes = frag::backward_workspace(plan, dtype, B, L);
+  if (use_frag(plan) || (ckpt_stride > 0 && use_jit(plan) && plan->frag.ok)) {
+    // checkpoint_stride on the fragment kernels (the generated kernels take none)
+    *bytes = frag::backward_workspace(plan, dtype, B, L, ckpt_stride);
     return SIGB_OK;
   }
   if (dtype == SIGB_F32) {
@@ -361,10 +362,10 @@ extern "C" int sigb_backward(const sigb_plan* plan, int dtype, const void* d_X, 
       return frag::backward(plan, dtype, d_X, B, L, d_S, s_ld, s_col0, d_g, g_ld, g_col0, d_work, work_bytes, d_dX,
                             d_dinc, (cudaStream_t)stream);
   }
-  if (use_frag(plan) && ckpt_stride == 0 && B > 0 && L > 1) {
+  if ((use_frag(plan) || (ckpt_stride > 0 && use_jit(plan) && plan->frag.ok)) && B > 0 && L > 1) {
     if (s_is_state) { s_ld = plan->Wc; s_col0 = 0; }
     return frag::backward(plan, dtype, d_X, B, L, d_S, s_ld, s_col0, d_g, g_ld, g_col0, d_work, work_bytes, d_dX,
-                          d_dinc, (cudaStream_t)stream);
+                          d_dinc, (cudaStream_t)stream, ckpt_stride);
   }
   if (dtype == SIGB_F32)
     return backward_t<float>(plan, d_X, B, L, d_S, s_ld, s_col0, s_is_state, d_g, g_ld, g_col0, ckpt_stride, d_work,

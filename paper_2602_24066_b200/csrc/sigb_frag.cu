@@ -42,9 +42,16 @@ int fwd(const sigb_plan* p, const T* X, int64_t B, int64_t L, const int64_t* bou
   return SIGB_OK;
 }
 
+// checkpoint rows per path (checkpoint_stride > 0): the chain and mid slots of every fragment at
+// k = 0, stride, 2 stride, ... (frag_ckpt_kernel)
+size_t ckpt_elems(const sigb_plan* p, int64_t L, int64_t stride, int NS) {
+  return stride > 0 ? (size_t)((L - 1) / stride + 1) * NS * p->frag.Fp : 0;
+}
+
 template <typename T>
-int64_t bwd_chunk(const sigb_plan* p, int64_t B, int64_t L) {
-  const size_t per_path = sizeof(T) * (size_t)p->frag.cpp * (size_t)(L - 1) * p->d;
+int64_t bwd_chunk(const sigb_plan* p, int64_t B, int64_t L, int64_t stride = 0) {
+  const size_t per_path = sizeof(T) * ((size_t)p->frag.cpp * (size_t)(L - 1) * p->d +
+                                       ckpt_elems(p, L, stride, p->frag.NC + p->frag.G));
   int64_t c = per_path ? (int64_t)(partial_budget() / 2 / per_path) : B;
   return std::max<int64_t>(1, std::min(c, B));
 }
@@ -73,23 +80,35 @@ __global__ void frag_sample_grads(const T* __restrict__ partial, int64_t Bc, int
 
 template <typename T, int NC, int G, int K>
 int bwd(const sigb_plan* p, const T* X, int64_t B, int64_t L, const T* S, int64_t s_ld, int64_t s_col0, const T* g,
-        int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, T* dX, T* dinc, cudaStream_t stream) {
+        int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, T* dX, T* dinc, cudaStream_t stream,
+        int64_t stride) {
   const int d = (int)p->d;
   const int64_t M = L - 1;
   const int cpp = p->frag.cpp;
-  const int64_t chunk = bwd_chunk<T>(p, B, L);
-  const size_t need = sizeof(T) * (size_t)chunk * cpp * M * d;
+  const int64_t chunk = bwd_chunk<T>(p, B, L, stride);
+  const size_t part = (size_t)chunk * cpp * M * d;
+  const size_t need = sizeof(T) * (part + (size_t)chunk * ckpt_elems(p, L, stride, NC + G));
   if (!work || work_bytes < need) return fail(SIGB_ERR_DOMAIN, "backward workspace too small");
   const size_t smem = sizeof(T) * bwd_smem_elems<NC, G, K>(d, p->frag.pstride);
-  SIGB_CUDA_TRY(cudaFuncSetAttribute(frag_backward_kernel<T, NC, G, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
+  auto kern = stride > 0 ? frag_backward_kernel<T, NC, G, K, true> : frag_backward_kernel<T, NC, G, K, false>;
+  SIGB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const size_t csmem = sizeof(T) * (2 * (size_t)(kChunkF + 1) * d + (size_t)kChunkF * (d + 1));
+  if (stride > 0 && csmem > 48 * 1024)
+    SIGB_CUDA_TRY(cudaFuncSetAttribute(frag_ckpt_kernel<T, NC, G, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)csmem));
   T* partial = (T*)work;
+  T* ckpt = stride > 0 ? partial + part : nullptr;
   for (int64_t b0 = 0; b0 < B; b0 += chunk) {
     const int64_t Bc = std::min(chunk, B - b0);
+    if (stride > 0) {
+      count_launch();
+      frag_ckpt_kernel<T, NC, G, K><<<(unsigned)(Bc * cpp), kTPB, csmem, stream>>>(dev_of(p), X, L, b0, stride, ckpt);
+      SIGB_CUDA_TRY(cudaGetLastError());
+    }
     count_launch(2);
     timing_begin(1, stream);
-    frag_backward_kernel<T, NC, G, K><<<(unsigned)(Bc * cpp), kTPB, smem, stream>>>(dev_of(p), X, L, b0, S, s_ld,
-                                                                                    s_col0, g, g_ld, g_col0, partial);
+    kern<<<(unsigned)(Bc * cpp), kTPB, smem, stream>>>(dev_of(p), X, L, b0, S, s_ld, s_col0, g, g_ld, g_col0, partial,
+                                                       ckpt, stride);
     timing_end(1, stream);
     SIGB_CUDA_TRY(cudaGetLastError());
     const int64_t n = Bc * L * d;
@@ -128,23 +147,24 @@ int forward(const sigb_plan* p, int dtype, const void* Xv, int64_t B, int64_t L,
   return fail(SIGB_ERR_UNSUPPORTED, "no fragment kernel for this shape");
 }
 
-size_t backward_workspace(const sigb_plan* p, int dtype, int64_t B, int64_t L) {
+size_t backward_workspace(const sigb_plan* p, int dtype, int64_t B, int64_t L, int64_t stride) {
   const size_t es = dtype == SIGB_F32 ? 4 : 8;
-  const int64_t chunk = dtype == SIGB_F32 ? bwd_chunk<float>(p, B, L) : bwd_chunk<double>(p, B, L);
-  return es * (size_t)chunk * p->frag.cpp * (size_t)(L - 1) * p->d;
+  const int64_t chunk = dtype == SIGB_F32 ? bwd_chunk<float>(p, B, L, stride) : bwd_chunk<double>(p, B, L, stride);
+  return es * (size_t)chunk *
+         ((size_t)p->frag.cpp * (size_t)(L - 1) * p->d + ckpt_elems(p, L, stride, p->frag.NC + p->frag.G));
 }
 
 int backward(const sigb_plan* p, int dtype, const void* Xv, int64_t B, int64_t L, const void* S, int64_t s_ld,
              int64_t s_col0, const void* g, int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, void* dX,
-             void* dinc, cudaStream_t stream) {
+             void* dinc, cudaStream_t stream, int64_t stride) {
   const int NC = p->frag.NC, G = p->frag.G, K = p->frag.K;
 #define X(a, b, c)                                                                                                 \
   if (NC == a && G == b && K == c) {                                                                               \
     if (dtype == SIGB_F32)                                                                                         \
       return bwd<float, a, b, c>(p, (const float*)Xv, B, L, (const float*)S, s_ld, s_col0, (const float*)g, g_ld,  \
-                                 g_col0, work, work_bytes, (float*)dX, (float*)dinc, stream);                      \
+                                 g_col0, work, work_bytes, (float*)dX, (float*)dinc, stream, stride);              \
     return bwd<double, a, b, c>(p, (const double*)Xv, B, L, (const double*)S, s_ld, s_col0, (const double*)g,      \
-                                g_ld, g_col0, work, work_bytes, (double*)dX, (double*)dinc, stream);               \
+                                g_ld, g_col0, work, work_bytes, (double*)dX, (double*)dinc, stream, stride);       \
   }
   SIGB_FRAG_CASES(X)
 #undef X

@@ -277,6 +277,52 @@ __global__ void __launch_bounds__(kTPB) frag_forward_kernel(FragDev fd, const T*
   if (orow && include_empty && f == 0) orow[-1] = T(1);
 }
 
+// Checkpoint replay for checkpoint_stride > 0 (reference backward.py:183-199, _kernels.py:122-141):
+// the fragment forward without its leaves, storing every fragment's chain and mid values
+// S_{0,t_k} at k = 0, stride, 2 stride, ... into ckpt[path][k / stride][slot][fragment] (slot-major:
+// a warp's stores are coalesced).  The backward reloads them instead of its exp(-dX)
+// reconstruction at those steps (frag_backward_kernel, CK).
+template <typename T, int NC, int G, int K>
+__global__ void __launch_bounds__(kTPB) frag_ckpt_kernel(FragDev fd, const T* __restrict__ X, int64_t L, int64_t b0,
+                                                         int64_t stride, T* __restrict__ ckpt) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Xs = reinterpret_cast<T*>(smem_raw);
+  T* Dl = Xs + (kChunkF + 1) * fd.d;
+  const int64_t bl = blockIdx.x / fd.cpp, b = b0 + bl;
+  const int f = (int)(blockIdx.x % fd.cpp) * kTPB + threadIdx.x;
+  Letters<NC, G, K> lt;
+  load_letters<NC, G, K>(fd, f, lt);
+  FState<T, NC, G, K> st;
+  for_slots<T, NC, G, K>(st, [&](int i, T& v) { v = fd.cidx[(size_t)i * fd.Fp + f] == -2 ? T(1) : T(0); });
+  const int64_t M = L - 1, nck = M / stride + 1;
+  constexpr int NS = NC + G;  // the slots the backward reloads
+  T* cb = ckpt + bl * nck * NS * fd.Fp + f;
+  auto store = [&](int64_t k) {
+    T* row = cb + k * NS * fd.Fp;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) row[(size_t)c * fd.Fp] = st.ch[c];
+#pragma unroll
+    for (int g = 0; g < G; ++g) row[(size_t)(NC + g) * fd.Fp] = st.mid[g];
+  };
+  store(0);
+  const T* Xb = X + b * L * fd.d;
+  T* Xs2 = Dl + kChunkF * (fd.d + 1);  // second sample buffer
+  if (M > 0) issue_rows<T>(Xb, fd.d, 0, (int)(M < kChunkF ? M : kChunkF), Xs);
+  for (int64_t j0 = 0, c = 0; j0 < M; j0 += kChunkF, ++c) {
+    const int cs = (int)(M - j0 < kChunkF ? M - j0 : kChunkF);
+    T* Xc = (c & 1) ? Xs2 : Xs;
+    diff_rows<T>(Xc, fd.d, cs, Dl);
+    const int64_t j1 = j0 + kChunkF;
+    if (j1 < M) issue_rows<T>(Xb, fd.d, (int)j1, (int)(M - j1 < kChunkF ? M - j1 : kChunkF), (c & 1) ? Xs : Xs2);
+    for (int s = 0; s < cs; ++s) {
+      FIncr<T, NC, G, K> in;
+      gather<T, NC, G, K>(Dl + s * (fd.d + 1), lt, T(1), in);
+      chen_step<T, NC, G, K, false>(st, in);
+      if ((j0 + s + 1) % stride == 0) store((j0 + s + 1) / stride);
+    }
+  }
+}
+
 // 16-byte aligned shared-memory load of four consecutive elements.
 __device__ __forceinline__ void load4(const float* p, float& a, float& b, float& c, float& d) {
   const float4 v = *reinterpret_cast<const float4*>(p);
@@ -296,11 +342,12 @@ __host__ __device__ constexpr size_t bwd_smem_elems(int d, int pstride) {
 
 // Backward over paths [b0, b0 + gridDim.x / cpp).  partial layout:
 // [(b - b0) * cpp + cip][M][d] (fixed-order sums of this CTA's fragments).
-template <typename T, int NC, int G, int K>
+template <typename T, int NC, int G, int K, bool CK = false>
 __global__ void __launch_bounds__(kTPB) frag_backward_kernel(FragDev fd, const T* __restrict__ X, int64_t L,
                                                              int64_t b0, const T* __restrict__ Sin, int64_t s_ld,
                                                              int64_t s_col0, const T* __restrict__ gup,
-                                                             int64_t g_ld, int64_t g_col0, T* __restrict__ partial) {
+                                                             int64_t g_ld, int64_t g_col0, T* __restrict__ partial,
+                                                             const T* __restrict__ ckpt = nullptr, int64_t stride = 0) {
   using SH = Shape<NC, G, K>;
   constexpr int NV = SH::NV;
   constexpr int NGS = SH::NGS;
@@ -343,6 +390,28 @@ __global__ void __launch_bounds__(kTPB) frag_backward_kernel(FragDev fd, const T
   T* pout = partial + (bl * fd.cpp + cip) * M * d;
   const int nchunks = (int)((M + kChunkF - 1) / kChunkF);
   T* Xs2 = buf + (size_t)kRedSteps * fd.pstride;  // second sample buffer
+  // checkpoint_stride (CK): the chain / mid values of the next checkpoint at or below the current
+  // step, prefetched one reload ahead; ck_rem = j mod stride and ck_k = j / stride are carried down
+  // the sweep (no 64-bit division per step)
+  T ck_ch[NC], ck_mid[G];
+  int ck_rem = 0;
+  int64_t ck_k = 0;
+  const T* ck_base = nullptr;
+  auto ck_load = [&](int64_t k) {
+    const T* row = ck_base + k * (NC + G) * fd.Fp;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) ck_ch[c] = row[(size_t)c * fd.Fp];
+#pragma unroll
+    for (int g = 0; g < G; ++g) ck_mid[g] = row[(size_t)(NC + g) * fd.Fp];
+  };
+  if constexpr (CK) {
+    if (M > 0) {
+      ck_rem = (int)((M - 1) % stride);  // the sweep's first step j = M - 1
+      ck_k = (M - 1) / stride;
+      ck_base = ckpt + bl * (M / stride + 1) * (NC + G) * fd.Fp + f;
+      ck_load(ck_k);
+    }
+  }
   if (nchunks > 0) issue_rows<T>(Xb, d, (nchunks - 1) * kChunkF, (int)(M - (nchunks - 1) * kChunkF), Xs);
   for (int c = nchunks - 1; c >= 0; --c) {
     const int j0 = c * kChunkF;
@@ -358,6 +427,19 @@ __global__ void __launch_bounds__(kTPB) frag_backward_kernel(FragDev fd, const T
       // (a) S_{0,t_{j+1}} -> S_{0,t_j} (chain and mids; leaf values are never read)
       gather<T, NC, G, K>(row, lt, T(-1), in);
       chen_step<T, NC, G, K, false>(st, in);
+      if constexpr (CK) {  // S_{0,t_j} from the forward replay at the checkpoint steps
+        if (ck_rem == 0) {
+#pragma unroll
+          for (int c = 0; c < NC; ++c) st.ch[c] = ck_ch[c];
+#pragma unroll
+          for (int g = 0; g < G; ++g) st.mid[g] = ck_mid[g];
+        }
+        const int nrem = ck_rem == 0 ? (int)stride - 1 : ck_rem - 1;
+        const int64_t nk = ck_rem == 0 ? ck_k - 1 : ck_k;
+        if (nrem == 0 && nk >= 0) ck_load(nk);
+        ck_rem = nrem;
+        ck_k = nk;
+      }
       // (b) forward partials from S_{0,t_j}
       gather<T, NC, G, K>(row, lt, T(1), in);
       T tch[NC][NC + 3];

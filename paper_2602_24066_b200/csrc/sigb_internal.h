@@ -224,10 +224,11 @@ bool supported(int NC, int G, int K);
 // bounds (K, 2) / K: windowed forward over B*K virtual paths (bounds NULL, K 1: whole paths)
 int forward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, const int64_t* bounds, int64_t K,
             void* out, int64_t out_ld, int64_t out_col0, int include_empty, void* state, cudaStream_t stream);
-size_t backward_workspace(const sigb_plan* p, int dtype, int64_t B, int64_t L);
+// stride > 0: checkpoint_stride (replay + reload, frag_ckpt_kernel); the workspace adds the rows
+size_t backward_workspace(const sigb_plan* p, int dtype, int64_t B, int64_t L, int64_t stride = 0);
 int backward(const sigb_plan* p, int dtype, const void* X, int64_t B, int64_t L, const void* S, int64_t s_ld,
              int64_t s_col0, const void* g, int64_t g_ld, int64_t g_col0, void* work, size_t work_bytes, void* dX,
-             void* dinc, cudaStream_t stream);
+             void* dinc, cudaStream_t stream, int64_t stride = 0);
 }  // namespace frag
 namespace trunc {
 bool supported(int64_t d, int depth);

@@ -180,3 +180,31 @@ def test_checkpoint_stride_truncated_kernels(stride):
         g2 = np.random.default_rng(7).standard_normal((2, len(w2)))
         _, d2 = ora.backward(X2, w2.codes, w2.lengths, w2.d, g2, stride=stride)
         assert ora.rel_err(sk.signature_backward(X2, w2, g2, checkpoint_stride=stride).path_grads, d2) <= TOL64
+
+
+@pytest.mark.parametrize("stride", [1, 3, 7])
+def test_checkpoint_stride_fragment_kernels(stride):
+    """checkpoint_stride on the fragment kernels (frag_ckpt_kernel replay + reload in
+    frag_backward_kernel): the c4 anisotropic set, a non-prefix-closed user set (closure state) and
+    the c3 trie (whose generated kernels take no checkpoints: the fragment kernels serve it), each
+    fp64 drop-in against the oracle's own stride-`stride` backward (1e-10) and stride 0 (1e-9, the
+    reference's test_backward.py:225-234 bar), fp32 autograd against the oracle (1e-4)."""
+    rng = np.random.default_rng(300 + stride)
+    sets = [("c4", build_wordset("c4", sk)), ("c3", build_wordset("c3", sk)),
+            ("non-closed", sk.build_custom([(0, 1, 1), (1,), (1, 0, 2), (2, 2, 2, 2), (0, 2), (3, 1, 0)], 4))]
+    for name, ws in sets:
+        if name == "c4":
+            assert ws.plan().kernel_kind == 2, name  # the fragment family serves the set
+        # (c3 and the small non-closed set plan the generated kernels, which take no checkpoints:
+        # their checkpointed backward runs on the fragment kernels too)
+        B, L = 3, 41
+        X = brownian(int(rng.integers(1 << 30)), B, L, ws.d)
+        g = rng.standard_normal((B, len(ws)))
+        ck = sk.signature_backward(X, ws, g, checkpoint_stride=stride).path_grads
+        plain = sk.signature_backward(X, ws, g).path_grads
+        _, dref = ora.backward(X, ws.codes, ws.lengths, ws.d, g, stride=stride)
+        assert ora.rel_err(ck, dref) <= TOL64, name
+        assert ora.rel_err(ck, plain) <= 1e-9, name
+        Xt = torch.from_numpy(X.astype(np.float32)).cuda().requires_grad_(True)
+        sk.signature(Xt, ws, checkpoint_stride=stride).backward(torch.from_numpy(g).float().cuda())
+        assert ora.rel_err(Xt.grad.cpu().numpy(), dref) <= TOL32, name
