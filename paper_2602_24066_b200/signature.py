@@ -292,8 +292,43 @@ def signature_forward(paths, ws: WordSet, threads: int | None = None) -> Coeffic
         return CoefficientBatch(ws, out)
     dev = resolve_device()
     X = to_device(paths.samples, dev)
-    out, _ = forward_tensor(X, ws)
-    return CoefficientBatch(ws, to_host(out))
+    return CoefficientBatch(ws, _forward_to_host(X, ws))
+
+
+# host results this large stream back in chunks, each copy under the next chunk's forward
+_PIPE_MIN_BYTES = 256 << 20
+_PIPE_CHUNK_BYTES = 128 << 20
+
+
+def _forward_to_host(X: torch.Tensor, ws: WordSet) -> np.ndarray:
+    """Forward of a device batch whose coefficients go back to host memory (the numpy drop-in).
+
+    Large results are computed in chunks of paths: chunk k's coefficients copy into one pinned
+    host array on a side stream while chunk k+1 computes, so the PCIe transfer (the drop-in's
+    bound: 4-8 bytes per word and path) overlaps the kernels.  The chunks take the sequential
+    route (the kernels are per path, so the values are bitwise those of one launch)."""
+    B, width, es = X.shape[0], ws.width, X.element_size()
+    plan = ws.plan(X.device)
+    if B < 2 or B * width * es < _PIPE_MIN_BYTES or _scan_segments(plan, ws, B, X.shape[1] - 1) > 1:
+        out, _ = forward_tensor(X, ws)
+        return to_host(out)
+    host = torch.empty((B, width), dtype=X.dtype, pin_memory=True)
+    per = max(1, _PIPE_CHUNK_BYTES // (width * es))
+    with torch.cuda.device(X.device):
+        main = torch.cuda.current_stream(X.device)
+        side = torch.cuda.Stream(X.device)
+        for lo in range(0, B, per):
+            hi = min(B, lo + per)
+            out = torch.empty((hi - lo, width), dtype=X.dtype, device=X.device)
+            plan.forward(X[lo:hi], out, 1 if ws.include_empty else 0, ws.include_empty, None)
+            ready = torch.cuda.Event()
+            ready.record(main)
+            with torch.cuda.stream(side):
+                side.wait_event(ready)
+                host[lo:hi].copy_(out, non_blocking=True)
+            out.record_stream(side)
+        side.synchronize()
+    return host.numpy()
 
 
 def signature_windows(paths, ws: WordSet, windows, threads: int | None = None) -> list[CoefficientBatch]:
