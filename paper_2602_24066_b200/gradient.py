@@ -152,10 +152,61 @@ def signature_backward(paths, ws: WordSet, upstream, threads: int | None = None,
         raise DomainError(f"checkpoint stride must be >= 1, got {checkpoint_stride}")
     dev = resolve_device(paths.samples.device if is_t and paths.samples.is_cuda else None)
     X = to_device(paths.samples, dev)
+    stride = int(checkpoint_stride or 0)
+    if not is_t and up.nbytes >= _PIPE_MIN_BYTES and paths.B > 1:
+        dX, dinc = _backward_host(X, ws, up, g_col0, stride)
+        return GradBatch(upstream=np.ascontiguousarray(up[:, g_col0:]), increment_grads=dinc, path_grads=dX)
     G = to_device(up, dev).contiguous()
-    dX, dinc = backward_tensor(X, ws, G, g_col0, int(checkpoint_stride or 0), want_inc=True)
+    dX, dinc = backward_tensor(X, ws, G, g_col0, stride, want_inc=True)
     up_words = up[:, g_col0:]
     if is_t:
         return GradBatch(upstream=up_words, increment_grads=dinc, path_grads=dX)
     return GradBatch(upstream=np.ascontiguousarray(up_words), increment_grads=to_host(dinc),
                      path_grads=to_host(dX))
+
+
+# a host upstream this large streams in chunks of paths (_backward_host)
+_PIPE_MIN_BYTES = 256 << 20
+_PIPE_CHUNK_BYTES = 128 << 20
+
+
+def _backward_host(X: torch.Tensor, ws: WordSet, up: np.ndarray, g_col0: int, stride: int):
+    """The numpy drop-in backward in chunks of paths.  The upstream (8 bytes per word and path: the
+    drop-in's dominant transfer) is staged chunk by chunk into two pinned buffers while the
+    device runs the previous chunk, each chunk's H2D runs on a side stream, and the gradients
+    land in pinned host arrays behind the chunk's kernels.  Paths are independent in the
+    kernels, so the values are bitwise those of one launch."""
+    dev = X.device
+    B, L, d = X.shape
+    per = max(1, _PIPE_CHUNK_BYTES // max(1, up.shape[1] * up.itemsize))
+    up_t = torch.from_numpy(up)
+    dX_h = torch.empty((B, L, d), dtype=X.dtype, pin_memory=True)
+    dinc_h = torch.empty((B, max(L - 1, 0), d), dtype=X.dtype, pin_memory=True)
+    stage = [torch.empty((per, up.shape[1]), dtype=up_t.dtype, pin_memory=True) for _ in range(2)]
+    with torch.cuda.device(dev):
+        main = torch.cuda.current_stream(dev)
+        h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        staged = [None, None]  # events: the H2D out of stage[i] is done (the buffer may be refilled)
+        for k, lo in enumerate(range(0, B, per)):
+            hi, i = min(B, lo + per), k % 2
+            if staged[i] is not None:
+                staged[i].synchronize()
+            stage[i][: hi - lo].copy_(up_t[lo:hi])  # host: overlaps the device work queued so far
+            with torch.cuda.stream(h2d):
+                G = torch.empty((hi - lo, up.shape[1]), dtype=X.dtype, device=dev)
+                G.copy_(stage[i][: hi - lo], non_blocking=True)
+                staged[i] = torch.cuda.Event()
+                staged[i].record(h2d)
+            main.wait_event(staged[i])
+            G.record_stream(main)
+            dX, dinc = backward_tensor(X[lo:hi], ws, G, g_col0, stride, want_inc=True)
+            done = torch.cuda.Event()
+            done.record(main)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(done)
+                dX_h[lo:hi].copy_(dX, non_blocking=True)
+                dinc_h[lo:hi].copy_(dinc, non_blocking=True)
+            dX.record_stream(d2h)
+            dinc.record_stream(d2h)
+        d2h.synchronize()
+    return dX_h.numpy(), dinc_h.numpy()

@@ -31,3 +31,28 @@ def test_chunked_numpy_forward_bitwise(name, monkeypatch):
     chunked = sk.signature_forward(X, ws).values
     assert isinstance(chunked, np.ndarray)
     assert np.array_equal(chunked, whole)
+
+
+@pytest.mark.parametrize("name", ["c5", "c4", "c3", "non-closed", "eps"])
+@pytest.mark.parametrize("stride", [0, 3])
+def test_chunked_numpy_backward_bitwise(name, stride, monkeypatch):
+    """gradient._backward_host (upstream staged in chunks through pinned buffers) against one launch
+    on device tensors: path and increment gradients bitwise equal."""
+    gradmod = importlib.import_module("paper_2602_24066_b200.gradient")
+    if name == "non-closed":
+        ws = sk.build_custom([(0, 1, 1), (1,), (1, 0, 2), (2, 2, 2, 2), (0, 2), (3, 1, 0)], 4)
+    elif name == "eps":
+        ws = sk.build_truncated(8, 4, include_empty=True)
+    else:
+        ws = build_wordset(name, sk)
+    B, L = 23, 29
+    X = brownian(19, B, L, ws.d)
+    g = np.random.default_rng(20).standard_normal((B, ws.width))
+    kw = {"checkpoint_stride": stride} if stride else {}
+    ref = sk.signature_backward(torch.from_numpy(X).cuda(), ws, torch.from_numpy(g).cuda(), **kw)
+    monkeypatch.setattr(gradmod, "_PIPE_MIN_BYTES", 1)
+    monkeypatch.setattr(gradmod, "_PIPE_CHUNK_BYTES", 4 * ws.width * 8)  # 4-path chunks, ragged tail
+    got = sk.signature_backward(X, ws, g, **kw)
+    assert isinstance(got.path_grads, np.ndarray)
+    assert np.array_equal(got.path_grads, ref.path_grads.cpu().numpy())
+    assert np.array_equal(got.increment_grads, ref.increment_grads.cpu().numpy())
