@@ -26,21 +26,22 @@
 // A1 rows = parents u (K = z), A2 rows = (gp, z) pairs (K = y), both constant
 // over the sweep and written to shared memory once; B = the chunk's increments
 // (K = letter, N = step), rebuilt per chunk.  fp32 accuracy from a scaled 3-pass
-// fp16 split (A rows per thread and B columns per step scaled by powers of two
-// into [2^13, 2^14), x = hi + lo, D = A_hi B_hi + A_lo B_hi + A_hi B_lo;
-// tools/ubench_tc_f16.cu: 7.6e-8 relative).  Steps 16-31 and 0-15 of a chunk
-// are two MMA groups with their own mbarrier, so the second group runs while
-// the sweep walks the first.  TMEM: {D1, D2} x 8 tiles x 16 steps x 2 groups =
-// 512 columns; one CTA (a quarter path: 64 grand-parents x 4 letter quads) per
-// SM (152 KB shared memory).
+// fp16 split (A rows scaled per grand-parent at depth 4, per thread at depth 5, and
+// B columns per step, by powers of two into [2^13, 2^14), x = hi + lo,
+// D = A_hi B_hi + A_lo B_hi + A_hi B_lo; tools/ubench_tc_f16.cu: 7.6e-8 relative).
+// Steps 16-31 and 0-15 of a chunk are two MMA groups with their own mbarrier, so
+// the second group runs while the sweep walks the first.  TMEM: {D1, D2} x 8 tiles
+// x 16 steps x 2 groups = 512 columns; one CTA (a quarter path) per SM (220 KB of
+// shared memory at depth 4).
 //
-// Thread (grand-parent gp, quad q) owns: the chain of gp (levels 1-2, computed
-// redundantly by the quad), parents gp.y for y in 4q..4q+3 (state, adjoint, D1
-// rows) and pairs (gp, z) for z in 4q..4q+3 (P state, D2 rows).  Its letter sums
-// for the quad's four letters (parent terms + leaf terms + chain terms) are
-// reduced over the warp's 8 grand-parents by a 4-shuffle transposing butterfly,
-// parked per warp in shared memory, and summed over the 8 warps in fixed order
-// per chunk into the partial buffer trunc_sample_grads telescopes.
+// Thread (grand-parent gp, letter quad q) owns: parents gp.y for y in the quad's
+// letters (adjoint, D1 rows) and pairs (gp, z) for z in them (P state, D2 rows).
+// At depth 4 the grand-parent's chain is walked once per warp and MMA group
+// (chain_pre) and its reverse mode deferred to a per-chunk sweep (chain_sweep);
+// at depth 5 the quad computes the chain in the step.  The letter sums of the
+// quad's letters are reduced over the warp's grand-parents by a transposing
+// shuffle butterfly, parked per warp in shared memory, and summed over the 8 warps
+// in fixed order per chunk into the partial buffer trunc_sample_grads telescopes.
 #pragma once
 
 #include "sigb_tc_util.cuh"
