@@ -128,15 +128,30 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
       else asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncwarp();
       const int cs = chunk_len(c), db = c & 1;
-      const float* xs = Xsb(db);
-      float* dl = Dlb(db);
-      for (int i = lane; i < CH * D; i += 32) dl[i] = i < cs * D ? xs[i + D] - xs[i] : 0.f;
-      __syncwarp();
-      for (int i = lane; i < CH * D; i += 32) {  // B[r]: rows = letters (hi 0-15, lo in its own tile), K = 8 steps
-        const int sidx = i / D, n = i % D, r = sidx / kStepsPerMma, k = sidx % kStepsPerMma;
-        const float x = dl[i], h = tf32_hi(x);
-        Bsb(db, r, 0)[kmajor_off(n, k)] = h;
-        Bsb(db, r, 1)[kmajor_off(n, k)] = x - h;
+      // one pass over float4s (a step's four letters): increments into Dl, and their hi / lo
+      // split into the round's B operand (rows = letters, hi 0-15 and lo in its own tile, K = 8
+      // steps); steps past the chunk are zero.  (~110 instructions per lane per chunk: the
+      // stager shares its scheduler with four compute warps and must stay a chunk ahead.)
+      const float4* xs4 = reinterpret_cast<const float4*>(Xsb(db));
+      float4* dl4 = reinterpret_cast<float4*>(Dlb(db));
+      for (int i = lane; i < CH * D / 4; i += 32) {
+        const int sidx = i / (D / 4), n0 = (i % (D / 4)) * 4, r = sidx / kStepsPerMma, k = sidx % kStepsPerMma;
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (sidx < cs) {
+          const float4 a = xs4[i + D / 4], b = xs4[i];
+          x = make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);
+        }
+        dl4[i] = x;
+        float* bh = Bsb(db, r, 0);
+        float* bl = Bsb(db, r, 1);
+        const float v[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int off = kmajor_off(n0 + j, k);
+          const float h = tf32_hi(v[j]);
+          bh[off] = h;
+          bl[off] = v[j] - h;
+        }
       }
       tcu::fence_async_smem();
       asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(su32(&mbar[1 + db])) : "memory");
