@@ -119,8 +119,13 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
       const int rows = chunk_len(c) + 1;
       const float* src = X + (bpath * L + (int64_t)c * CH) * D;
       float* dst = Xsb(c & 1);
-      for (int i = lane; i < rows * D; i += 32)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(su32(dst + i)), "l"(src + i) : "memory");
+      if (((uintptr_t)src & 15) == 0) {  // rows of D floats: 16-byte copies when X is 16-byte aligned
+        for (int i = 4 * lane; i < rows * D; i += 128)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst + i)), "l"(src + i) : "memory");
+      } else {
+        for (int i = lane; i < rows * D; i += 32)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(su32(dst + i)), "l"(src + i) : "memory");
+      }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
     auto prepare = [&](int c, bool newest_in_flight) {  // Dl and the 4 rounds' B of chunk c, then "ready"
