@@ -235,13 +235,21 @@ __global__ void __launch_bounds__(kThreadsTc, 2)
 #pragma unroll
           for (int k = 0; k < NC; ++k) ch[k] = tch[k][k + 1];
           const float tNh = 0.5f * tN;  // dX/2 . T(gp, N) as dX . (T(gp, N)/2): exact, one scaling per step
+          // two parents per packed f32x2 FMA: (dX_g, dX_g+1) . T/2 + (S_g, S_g+1) gives their
+          // T(u, N) (the leaves' multipliers), . T(gp, N-1) their update (the pairs stay in the
+          // layout of the float4 increment load and of the state)
 #pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const float tm = fmaf(in.dy[g], tNh, mid[g]);  // T(u_g, N): the leaves' multiplier
-            mid[g] = fmaf(in.dy[g], tN1, mid[g]);
-            const float h = tf32_hi(tm);
-            ah[g][s] = h;
-            al[g][s] = tm - h;
+          for (int g = 0; g < G; g += 2) {
+            const float2 dy2 = make_float2(in.dy[g], in.dy[g + 1]), m2 = make_float2(mid[g], mid[g + 1]);
+            const float2 tm = __ffma2_rn(dy2, make_float2(tNh, tNh), m2);
+            const float2 nm = __ffma2_rn(dy2, make_float2(tN1, tN1), m2);
+            mid[g] = nm.x;
+            mid[g + 1] = nm.y;
+            const float h0 = tf32_hi(tm.x), h1 = tf32_hi(tm.y);
+            ah[g][s] = h0;
+            ah[g + 1][s] = h1;
+            al[g][s] = tm.x - h0;
+            al[g + 1][s] = tm.y - h1;
           }
         }
         if (c > 0) mbar_wait(&mbar[0], (uint32_t)((c - 1) & 1));  // round c-1's MMAs have read A
