@@ -116,6 +116,19 @@ __device__ __forceinline__ void chen_step(FState<T, NC, G, K>& st, const FIncr<T
 #pragma unroll
   for (int k = 0; k < NC; ++k) st.ch[k] = tch[k][k + 1];
   const T tNh = tN * T(0.5);  // dX/2 . T(anchor, NV) as dX . (T/2): exact, one scaling per step
+  if constexpr (!Leaves && sizeof(T) == 4) {
+    // the backward's reconstruction (no leaves): two mids' S += dX . T(anchor, NV-1) per packed
+    // f32x2 FMA
+#pragma unroll
+    for (int g = 0; g + 1 < G; g += 2) {
+      const float2 n2 = __ffma2_rn(make_float2(in.dy[g], in.dy[g + 1]), make_float2(tN1, tN1),
+                                   make_float2(st.mid[g], st.mid[g + 1]));
+      st.mid[g] = n2.x;
+      st.mid[g + 1] = n2.y;
+    }
+    if constexpr (G % 2) st.mid[G - 1] = fma(in.dy[G - 1], tN1, st.mid[G - 1]);
+    return;
+  }
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     if constexpr (Leaves) {
