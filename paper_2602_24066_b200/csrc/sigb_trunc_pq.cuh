@@ -634,7 +634,11 @@ __global__ void __launch_bounds__(kBlock, 1)
       float4 w[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) w[k] = reinterpret_cast<const float4*>(&red[db][k][0][0])[i];
-      auto add = [](float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); };
+      auto add = [](float4 a, float4 b) {  // two packed f32x2 adds (the producer shares a scheduler)
+        const float2 lo = __fadd2_rn(make_float2(a.x, a.y), make_float2(b.x, b.y));
+        const float2 hi = __fadd2_rn(make_float2(a.z, a.w), make_float2(b.z, b.w));
+        return make_float4(lo.x, lo.y, hi.x, hi.y);
+      };
       dst[i] = add(add(add(w[0], w[1]), add(w[2], w[3])), add(add(w[4], w[5]), add(w[6], w[7])));
     }
   };
