@@ -145,10 +145,17 @@ __device__ __forceinline__ void split_f16(float x, __half& hi, __half& lo) {
 }
 
 // 8 scaled fp32 values -> one 16-byte row of hi and one of lo core-matrix data
+// (pairs: packed f32x2 scale and residual, paired f32 -> f16x2 conversions; the same roundings
+// as split_f16 per value)
 __device__ __forceinline__ void split8_store(const float (&v)[8], float scale, __half* hi_dst, __half* lo_dst) {
-  __align__(16) __half h[8], l[8];
+  __align__(16) __half2 h[4], l[4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) split_f16(v[i] * scale, h[i], l[i]);
+  for (int i = 0; i < 4; ++i) {
+    const float2 x = __fmul2_rn(make_float2(v[2 * i], v[2 * i + 1]), make_float2(scale, scale));
+    h[i] = __float22half2_rn(x);
+    const float2 b = __half22float2(h[i]);
+    l[i] = __float22half2_rn(__fadd2_rn(x, make_float2(-b.x, -b.y)));
+  }
   *reinterpret_cast<uint4*>(hi_dst) = *reinterpret_cast<const uint4*>(h);
   *reinterpret_cast<uint4*>(lo_dst) = *reinterpret_cast<const uint4*>(l);
 }
