@@ -94,9 +94,23 @@ size_t bwd_workspace(int64_t B, int64_t L, int64_t stride = 0) {
 // A thread walks kSeg consecutive samples of one (path, channel), so each dInc is summed once
 // (the per-sample form summed every increment twice); same arithmetic, same bits.
 constexpr int kSeg = 32;
+// 16-byte vectors of the partial / gradient rows (d is 4, 8 or 16 here): 4 floats or 2 doubles
+template <typename T> struct Vec16;
+template <> struct Vec16<float> { using V = float4; static constexpr int W = 4; };
+template <> struct Vec16<double> { using V = double2; static constexpr int W = 2; };
+__device__ __forceinline__ float4 vadd(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+__device__ __forceinline__ float4 vsub(float4 a, float4 b) { return make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w); }
+__device__ __forceinline__ double2 vadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 vsub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+template <typename V> __device__ __forceinline__ V vzero();
+template <> __device__ __forceinline__ float4 vzero<float4>() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+template <> __device__ __forceinline__ double2 vzero<double2>() { return make_double2(0.0, 0.0); }
+
+// Scalar fallback for buffers the caller did not 16-byte align: thread = (path, segment, letter)
 template <typename T>
-__global__ void trunc_sample_grads(const T* __restrict__ partial, int64_t Bc, int64_t P, int64_t M, int64_t d,
-                                   int64_t b0, int64_t B, T* __restrict__ dX, T* __restrict__ dinc) {
+__global__ void trunc_sample_grads_scalar(const T* __restrict__ partial, int64_t Bc, int64_t P, int64_t M,
+                                          int64_t d, int64_t b0, int64_t B, T* __restrict__ dX,
+                                          T* __restrict__ dinc) {
   const int64_t L = M + 1, nseg = (L + kSeg - 1) / kSeg;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= Bc * nseg * d) return;
@@ -110,8 +124,7 @@ __global__ void trunc_sample_grads(const T* __restrict__ partial, int64_t Bc, in
   const int64_t t0 = sg * kSeg, t1 = t0 + kSeg < L ? t0 + kSeg : L;
   T prev = t0 >= 1 ? inc(t0 - 1) : T(0);
   for (int64_t t = t0; t < t1; ++t) {
-    T v = T(0);
-    if (t >= 1) v += prev;
+    T v = t >= 1 ? prev : T(0);
     if (t < M) {
       const T it = inc(t);
       v -= it;
@@ -119,6 +132,40 @@ __global__ void trunc_sample_grads(const T* __restrict__ partial, int64_t Bc, in
       prev = it;
     }
     dX[((b0 + bl) * L + t) * d + z] = v;
+  }
+}
+
+// dX[t] = inc(t-1) - inc(t), inc(j) = sum over the path's CTA parts of partial[part][j] (fixed
+// part order); thread = (path, 32-sample segment, 16-byte group of letters), vector loads/stores
+template <typename T>
+__global__ void trunc_sample_grads(const T* __restrict__ partial, int64_t Bc, int64_t P, int64_t M, int64_t d,
+                                   int64_t b0, int64_t B, T* __restrict__ dX, T* __restrict__ dinc) {
+  using V = typename Vec16<T>::V;
+  constexpr int W = Vec16<T>::W;
+  const int64_t L = M + 1, nseg = (L + kSeg - 1) / kSeg, dv = d / W;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= Bc * nseg * dv) return;
+  const int64_t zv = i % dv, sg = (i / dv) % nseg, bl = i / (dv * nseg);
+  if (b0 + bl >= B) return;
+  const V* pv = reinterpret_cast<const V*>(partial);
+  auto inc = [&](int64_t j) {
+    V s = vzero<V>();
+    for (int64_t p = 0; p < P; ++p) s = vadd(s, pv[((bl * P + p) * M + j) * dv + zv]);
+    return s;
+  };
+  V* xv = reinterpret_cast<V*>(dX);
+  V* iv = reinterpret_cast<V*>(dinc);
+  const int64_t t0 = sg * kSeg, t1 = t0 + kSeg < L ? t0 + kSeg : L;
+  V prev = t0 >= 1 ? inc(t0 - 1) : vzero<V>();
+  for (int64_t t = t0; t < t1; ++t) {
+    V v = t >= 1 ? prev : vzero<V>();
+    if (t < M) {
+      const V it = inc(t);
+      v = vsub(v, it);
+      if (dinc) iv[((b0 + bl) * M + t) * dv + zv] = it;
+      prev = it;
+    }
+    xv[((b0 + bl) * L + t) * dv + zv] = v;
   }
 }
 
@@ -186,9 +233,15 @@ int bwd(const T* X, int64_t B, int64_t L, const T* S, int64_t s_ld, int64_t s_co
     }
     timing_end(1, stream);
     SIGB_CUDA_TRY(cudaGetLastError());
-    const int64_t n = Bc * ((L + kSeg - 1) / kSeg) * D;
-    trunc_sample_grads<T><<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(partial, Bc, C::CPP, M, D, b0, B, dX,
-                                                                           dinc);
+    if ((((uintptr_t)partial | (uintptr_t)dX | (uintptr_t)dinc) & 15) == 0) {
+      const int64_t n = Bc * ((L + kSeg - 1) / kSeg) * (D / Vec16<T>::W);
+      trunc_sample_grads<T><<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(partial, Bc, C::CPP, M, D, b0, B, dX,
+                                                                             dinc);
+    } else {
+      const int64_t n = Bc * ((L + kSeg - 1) / kSeg) * D;
+      trunc_sample_grads_scalar<T><<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(partial, Bc, C::CPP, M, D, b0,
+                                                                                    B, dX, dinc);
+    }
     SIGB_CUDA_TRY(cudaGetLastError());
   }
   return SIGB_OK;
